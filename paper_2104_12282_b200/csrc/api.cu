@@ -1,0 +1,792 @@
+// libtomo host side: the C ABI of include/tomo.h.
+//
+// Host-only work at tomo_create (KE by quadrature and its Walsh-basis core, BC mask and
+// load list, filter taps); device work is enqueued on the stream bound by tomo_bind into
+// the caller's workspace. The PCG driver launches the fused K_A / K_B kernel pair per
+// iteration (kernels.cu) and reads the device scalars back once per batch of iterations.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/tomo.h"
+#include "tomo_internal.h"
+
+using namespace tomo;
+
+namespace tomo {
+int op_occupancy(int mode);
+}
+
+struct tomo_ctx {
+  Grid g{};
+  double h = 1, E0 = 1, Emin = 1e-9, nu = 0.3, penal = 3, rmin = 1.5;
+  double KE[576];
+  Walsh w{};
+  double ke_diag = 0;
+  std::vector<uint8_t> mask;       // per node, bit c = DOF 3n+c fixed
+  std::vector<int64_t> load_dofs;  // distinct, ascending insertion order
+  std::vector<double> load_vals;
+  double fnorm = 0;
+  std::vector<int> taps;  // 3 per tap
+  std::vector<double> tap_w;
+  std::string err;
+  // workspace
+  bool bound = false;
+  cudaStream_t st = nullptr;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  size_t off_E, off_dinv, off_Hs, off_t0, off_t1, off_u, off_r, off_p0, off_p1, off_q, off_us,
+      off_mask, off_cnt, off_ld, off_lv, off_taps, off_tw, off_part, off_scal, off_oc, off_end;
+  size_t n_part = 0;
+  int nchunk = 1;
+  dim3 opg;
+  int nb_b = 1, nb_s = 1, nb_oc = 1;
+  int64_t launches = 0;
+  int sms = 148;
+  // profiling
+  bool prof = false;
+  double prof_a_ms = 0, prof_b_ms = 0;
+  int64_t prof_n = 0;
+  std::vector<cudaEvent_t> ev;
+
+  template <class T>
+  T* P(size_t off) const { return reinterpret_cast<T*>(ws + off); }
+  double* E() const { return P<double>(off_E); }
+  double* dinv() const { return P<double>(off_dinv); }
+  double* Hs() const { return P<double>(off_Hs); }
+  double* t0() const { return P<double>(off_t0); }
+  double* t1() const { return P<double>(off_t1); }
+  double* u() const { return P<double>(off_u); }
+  double* r() const { return P<double>(off_r); }
+  double* p(int i) const { return P<double>(i ? off_p1 : off_p0); }
+  double* q() const { return P<double>(off_q); }
+  double* us() const { return P<double>(off_us); }
+  uint8_t* dmask() const { return P<uint8_t>(off_mask); }
+  int* cnt() const { return P<int>(off_cnt); }
+  int64_t* ld() const { return P<int64_t>(off_ld); }
+  double* lv() const { return P<double>(off_lv); }
+  int* dtaps() const { return P<int>(off_taps); }
+  double* tw() const { return P<double>(off_tw); }
+  double* part() const { return P<double>(off_part); }
+  Scal* scal() const { return P<Scal>(off_scal); }
+  double* ocout() const { return P<double>(off_oc); }
+};
+
+namespace {
+
+int fail(tomo_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(tomo_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, TOMO_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(ctx, expr)                                     \
+  do {                                                    \
+    cudaError_t _e = (expr);                              \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr); \
+  } while (0)
+
+#define LAUNCH(ctx, expr)  \
+  do {                     \
+    CK(ctx, (expr));       \
+    ++(ctx)->launches;     \
+  } while (0)
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---------------------------------------------------------------- KE by quadrature
+// KE = sum over the 2x2x2 Gauss points of w |J| B^T C B on a cube of edge h (SPEC.md
+// l.105-113): trilinear shape functions N_a = prod_d (x_d if corner_d else 1 - x_d) on
+// [0,1]^3, C isotropic (E = 1, nu), engineering shear strains. 2-point Gauss is exact here.
+void build_ke(double nu, double h, double* KE) {
+  static const int corner[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
+                                   {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
+  const double lam = nu / ((1 + nu) * (1 - 2 * nu)), mu = 1 / (2 * (1 + nu));
+  double C[6][6] = {};
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) C[a][b] = lam + (a == b ? 2 * mu : 0.0);
+  for (int a = 3; a < 6; ++a) C[a][a] = mu;
+  const double gp[2] = {0.5 - 0.5 / std::sqrt(3.0), 0.5 + 0.5 / std::sqrt(3.0)};
+  const double wdet = 0.125 * h * h * h;
+  std::memset(KE, 0, sizeof(double) * 576);
+  for (int p0 = 0; p0 < 2; ++p0)
+    for (int p1 = 0; p1 < 2; ++p1)
+      for (int p2 = 0; p2 < 2; ++p2) {
+        const double xi[3] = {gp[p0], gp[p1], gp[p2]};
+        double B[6][24] = {};
+        for (int a = 0; a < 8; ++a) {
+          double f[3], s[3];
+          for (int d = 0; d < 3; ++d) {
+            f[d] = corner[a][d] ? xi[d] : 1 - xi[d];
+            s[d] = corner[a][d] ? 1.0 : -1.0;
+          }
+          const double gx = s[0] * f[1] * f[2] / h, gy = f[0] * s[1] * f[2] / h,
+                       gz = f[0] * f[1] * s[2] / h;
+          B[0][3 * a] = gx;
+          B[1][3 * a + 1] = gy;
+          B[2][3 * a + 2] = gz;
+          B[3][3 * a] = gy; B[3][3 * a + 1] = gx;          // gamma_xy
+          B[4][3 * a + 1] = gz; B[4][3 * a + 2] = gy;      // gamma_yz
+          B[5][3 * a] = gz; B[5][3 * a + 2] = gx;          // gamma_zx
+        }
+        double CB[6][24];
+        for (int i = 0; i < 6; ++i)
+          for (int j = 0; j < 24; ++j) {
+            double acc = 0;
+            for (int k = 0; k < 6; ++k) acc += C[i][k] * B[k][j];
+            CB[i][j] = acc;
+          }
+        for (int i = 0; i < 24; ++i)
+          for (int j = 0; j < 24; ++j) {
+            double acc = 0;
+            for (int k = 0; k < 6; ++k) acc += B[k][i] * CB[k][j];
+            KE[24 * i + j] += wdet * acc;
+          }
+      }
+}
+
+// D = T KE T^T / 64 in the +-1 Walsh basis (mode m = mx + 2 my + 4 mz, sign +1 on the
+// corner side of each "difference" axis); extract the 7 coefficients and check that the
+// pattern reproduces all 576 entries.
+bool walsh_coefficients(const double* KE, Walsh* W, double* maxdev) {
+  static const int corner[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
+                                   {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
+  double T[8][8];
+  for (int m = 0; m < 8; ++m)
+    for (int a = 0; a < 8; ++a) {
+      double s = 1;
+      for (int d = 0; d < 3; ++d)
+        if ((m >> d) & 1) s *= corner[a][d] ? 1.0 : -1.0;
+      T[m][a] = s;
+    }
+  static double D[24][24];
+  for (int m = 0; m < 8; ++m)
+    for (int c = 0; c < 3; ++c)
+      for (int n = 0; n < 8; ++n)
+        for (int e = 0; e < 3; ++e) {
+          double acc = 0;
+          for (int a = 0; a < 8; ++a)
+            for (int b = 0; b < 8; ++b) acc += T[m][a] * KE[24 * (3 * a + c) + 3 * b + e] * T[n][b];
+          D[3 * m + c][3 * n + e] = acc / 64.0;
+        }
+  auto at = [&](int m, int c, int n, int e) { return D[3 * m + c][3 * n + e]; };
+  const int mx = 1, my = 2, mz = 4, mxy = 3, mxz = 5, myz = 6, mxyz = 7;
+  W->b = at(mx, 0, my, 1);
+  W->amb = at(mx, 0, mx, 0) - W->b;
+  W->g = at(mx, 1, mx, 1);
+  W->c1 = at(mxy, 0, mxy, 0);
+  W->c2 = at(mxy, 0, myz, 2);
+  W->c3 = at(mxy, 2, mxz, 1);
+  W->c4 = at(mxyz, 0, mxyz, 0);
+  double R[24][24] = {};
+  auto set = [&](int m, int c, int n, int e, double v) { R[3 * m + c][3 * n + e] += v; };
+  const int nm[3] = {mx, my, mz};
+  for (int c = 0; c < 3; ++c) {  // normal strains
+    for (int e = 0; e < 3; ++e) set(nm[c], c, nm[e], e, W->b);
+    set(nm[c], c, nm[c], c, W->amb);
+  }
+  for (int c = 0; c < 3; ++c)  // shear: v_{m_c, e} = v_{m_e, c} = g (w_{m_c,e} + w_{m_e,c})
+    for (int e = 0; e < 3; ++e)
+      if (c != e) {
+        set(nm[c], e, nm[c], e, W->g);
+        set(nm[c], e, nm[e], c, W->g);
+      }
+  // bilinear modes
+  set(mxy, 0, mxy, 0, W->c1); set(mxy, 0, myz, 2, W->c2);
+  set(mxy, 1, mxy, 1, W->c1); set(mxy, 1, mxz, 2, W->c2);
+  set(mxz, 0, mxz, 0, W->c1); set(mxz, 0, myz, 1, W->c2);
+  set(mxz, 2, mxz, 2, W->c1); set(mxz, 2, mxy, 1, W->c2);
+  set(myz, 1, myz, 1, W->c1); set(myz, 1, mxz, 0, W->c2);
+  set(myz, 2, myz, 2, W->c1); set(myz, 2, mxy, 0, W->c2);
+  const int sm[3] = {mxy, mxz, myz}, sc[3] = {2, 1, 0};
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) set(sm[i], sc[i], sm[j], sc[j], W->c3);
+    set(sm[i], sc[i], sm[i], sc[i], W->c3);
+  }
+  for (int c = 0; c < 3; ++c) set(mxyz, c, mxyz, c, W->c4);
+  double mx_abs = 0, dev = 0;
+  for (int i = 0; i < 24; ++i)
+    for (int j = 0; j < 24; ++j) {
+      mx_abs = std::fmax(mx_abs, std::fabs(D[i][j]));
+      dev = std::fmax(dev, std::fabs(D[i][j] - R[i][j]));
+    }
+  *maxdev = dev / mx_abs;
+  return dev <= 1e-13 * mx_abs;
+}
+
+inline long long node_id(const Grid& g, int i, int j, int k) {
+  return (long long)i + (long long)g.nnx * (j + (long long)g.nny * k);
+}
+
+bool check_ptr(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 7) == 0; }
+
+}  // namespace
+
+// ====================================================================== lifetime
+extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, double Emin,
+                           double nu, double penal, double rmin, const tomo_bc* bc) {
+  if (!out || !gr || !bc) return TOMO_EINVAL;
+  *out = nullptr;
+  tomo_ctx* c = new (std::nothrow) tomo_ctx();
+  if (!c) return TOMO_EINVAL;
+  auto bad = [&](const char* m) {
+    c->err = m;
+    *out = c;  // returned so tomo_last_error works; caller must destroy
+    return TOMO_EINVAL;
+  };
+  if (gr->nelx < 1 || gr->nely < 1 || gr->nelz < 1) return bad("nel* must be >= 1 (SPEC.md l.39)");
+  if (!(gr->h > 0)) return bad("h must be > 0");
+  if (!(Emin > 0 && Emin < E0)) return bad("need 0 < Emin < E0 (SPEC.md l.97)");
+  if (!(nu > 0 && nu < 0.5)) return bad("need 0 < nu < 0.5 (SPEC.md l.97)");
+  if (!(penal >= 1)) return bad("need penal >= 1 (SPEC.md l.97)");
+  if (!(rmin > 0)) return bad("need rmin > 0");
+  Grid& g = c->g;
+  g.nx = gr->nelx; g.ny = gr->nely; g.nz = gr->nelz;
+  g.nnx = g.nx + 1; g.nny = g.ny + 1; g.nnz = g.nz + 1;
+  g.nn = (long long)g.nnx * g.nny * g.nnz;
+  g.ne = (long long)g.nx * g.ny * g.nz;
+  g.ndof = 3 * g.nn;
+  if (g.ndof >= (1LL << 40)) return bad("grid too large");
+  c->h = gr->h; c->E0 = E0; c->Emin = Emin; c->nu = nu; c->penal = penal; c->rmin = rmin;
+  build_ke(nu, gr->h, c->KE);
+  double dev = 0;
+  if (!walsh_coefficients(c->KE, &c->w, &dev)) return bad("KE Walsh pattern check failed");
+  c->ke_diag = c->KE[0];
+  for (int i = 0; i < 24; ++i)
+    if (std::fabs(c->KE[25 * i] - c->ke_diag) > 1e-13 * c->ke_diag)
+      return bad("KE diagonal not constant");
+
+  // boundary conditions
+  c->mask.assign((size_t)g.nn, 0);
+  std::vector<std::pair<int64_t, double>> loads;
+  if (bc->kind == TOMO_BC_CANTILEVER) {
+    for (int k = 0; k <= g.nz; ++k)
+      for (int j = 0; j <= g.ny; ++j) c->mask[node_id(g, 0, j, k)] = 7;
+    for (int j = 0; j <= g.ny; ++j)
+      loads.push_back({3 * node_id(g, g.nx, j, 0) + 2, bc->load_total / (g.ny + 1)});
+  } else if (bc->kind == TOMO_BC_MBB_HALF) {
+    for (int k = 0; k <= g.nz; ++k)
+      for (int j = 0; j <= g.ny; ++j) c->mask[node_id(g, 0, j, k)] |= 1;
+    for (int j = 0; j <= g.ny; ++j) c->mask[node_id(g, g.nx, j, 0)] |= 4;
+    c->mask[node_id(g, g.nx, 0, 0)] |= 2;
+    for (int j = 0; j <= g.ny; ++j)
+      loads.push_back({3 * node_id(g, 0, j, g.nz) + 2, bc->load_total / (g.ny + 1)});
+  } else if (bc->kind == TOMO_BC_EXPLICIT) {
+    if (bc->n_fixed < 0 || bc->n_loads < 0) return bad("negative BC list length");
+    if ((bc->n_fixed && !bc->fixed_dofs) || (bc->n_loads && (!bc->load_dofs || !bc->load_vals)))
+      return bad("NULL BC list");
+    for (int64_t i = 0; i < bc->n_fixed; ++i) {
+      const int64_t d = bc->fixed_dofs[i];
+      if (d < 0 || d >= g.ndof) return bad("fixed DOF out of range");
+      c->mask[d / 3] |= (uint8_t)(1u << (d % 3));
+    }
+    for (int64_t i = 0; i < bc->n_loads; ++i) {
+      const int64_t d = bc->load_dofs[i];
+      if (d < 0 || d >= g.ndof) return bad("load DOF out of range");
+      loads.push_back({d, bc->load_vals[i]});
+    }
+  } else {
+    return bad("unknown BC kind");
+  }
+  for (auto& l : loads) {
+    if ((c->mask[l.first / 3] >> (l.first % 3)) & 1) return bad("a load sits on a fixed DOF (SPEC.md l.31)");
+    bool merged = false;
+    for (size_t i = 0; i < c->load_dofs.size(); ++i)
+      if (c->load_dofs[i] == l.first) { c->load_vals[i] += l.second; merged = true; break; }
+    if (!merged) { c->load_dofs.push_back(l.first); c->load_vals.push_back(l.second); }
+  }
+  double ff = 0;
+  for (double v : c->load_vals) ff += v * v;
+  c->fnorm = std::sqrt(ff);
+
+  // filter taps {d : rmin - |d| > 0}, order dz, dy, dx ascending (reading A15)
+  const int R = (int)std::ceil(rmin);
+  for (int dz = -R; dz <= R; ++dz)
+    for (int dy = -R; dy <= R; ++dy)
+      for (int dx = -R; dx <= R; ++dx) {
+        const double w = rmin - std::sqrt((double)(dx * dx + dy * dy + dz * dz));
+        if (w > 0) {
+          c->taps.push_back(dx); c->taps.push_back(dy); c->taps.push_back(dz);
+          c->tap_w.push_back(w);
+        }
+      }
+
+  // workspace layout
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
+  const size_t vd = sizeof(double) * (size_t)g.ndof, ve = sizeof(double) * (size_t)g.ne;
+  c->off_E = take(ve);
+  c->off_dinv = take(sizeof(double) * (size_t)g.nn);
+  c->off_Hs = take(ve);
+  c->off_t0 = take(ve);
+  c->off_t1 = take(ve);
+  c->off_u = take(vd);
+  c->off_r = take(vd);
+  c->off_p0 = take(vd);
+  c->off_p1 = take(vd);
+  c->off_q = take(vd);
+  c->off_us = take(vd);
+  c->off_mask = take((size_t)g.nn);
+  c->off_cnt = take(sizeof(int) * (size_t)g.ne);
+  c->off_ld = take(sizeof(int64_t) * (c->load_dofs.size() + 1));
+  c->off_lv = take(sizeof(double) * (c->load_dofs.size() + 1));
+  c->off_taps = take(sizeof(int) * (c->taps.size() + 3));
+  c->off_tw = take(sizeof(double) * (c->tap_w.size() + 1));
+  const dim3 og = op_grid(g, 1);
+  size_t maxb = (size_t)og.x * og.y * (size_t)std::min(g.nnz, 64);
+  c->n_part = std::max<size_t>(maxb, 8192) * 2;
+  c->off_part = take(sizeof(double) * c->n_part);
+  c->off_scal = take(sizeof(Scal));
+  c->off_oc = take(sizeof(double) * 4);
+  c->off_end = o;
+  *out = c;
+  return TOMO_OK;
+}
+
+extern "C" size_t tomo_workspace_bytes(const tomo_ctx* c) { return c ? c->off_end : 0; }
+
+extern "C" void tomo_destroy(tomo_ctx* c) {
+  if (!c) return;
+  for (auto e : c->ev) cudaEventDestroy(e);
+  delete c;
+}
+
+extern "C" const char* tomo_last_error(const tomo_ctx* c) {
+  return c ? c->err.c_str() : "null context";
+}
+
+extern "C" int tomo_sizes(const tomo_ctx* c, int64_t out[5]) {
+  if (!c || !out) return TOMO_EINVAL;
+  out[0] = c->g.ne; out[1] = c->g.nn; out[2] = c->g.ndof;
+  out[3] = (int64_t)c->load_dofs.size(); out[4] = (int64_t)c->tap_w.size();
+  return TOMO_OK;
+}
+
+extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
+  if (!c) return TOMO_EINVAL;
+  if (!d_ws || (reinterpret_cast<uintptr_t>(d_ws) & 255)) return fail(c, TOMO_EINVAL, "workspace must be 256-B aligned");
+  if (bytes < c->off_end) return fail(c, TOMO_ENOWORKSPACE, "workspace too small");
+  c->ws = static_cast<char*>(d_ws);
+  c->ws_bytes = bytes;
+  c->st = static_cast<cudaStream_t>(stream);
+  const Grid& g = c->g;
+  int dev = 0;
+  CK(c, cudaGetDevice(&dev));
+  CK(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(c, cudaMemcpyAsync(c->dmask(), c->mask.data(), (size_t)g.nn, cudaMemcpyHostToDevice, c->st));
+  if (!c->load_dofs.empty()) {
+    CK(c, cudaMemcpyAsync(c->ld(), c->load_dofs.data(), sizeof(int64_t) * c->load_dofs.size(), cudaMemcpyHostToDevice, c->st));
+    CK(c, cudaMemcpyAsync(c->lv(), c->load_vals.data(), sizeof(double) * c->load_vals.size(), cudaMemcpyHostToDevice, c->st));
+  }
+  if (!c->tap_w.empty()) {
+    CK(c, cudaMemcpyAsync(c->dtaps(), c->taps.data(), sizeof(int) * c->taps.size(), cudaMemcpyHostToDevice, c->st));
+    CK(c, cudaMemcpyAsync(c->tw(), c->tap_w.data(), sizeof(double) * c->tap_w.size(), cudaMemcpyHostToDevice, c->st));
+  }
+  CK(c, cudaMemsetAsync(c->scal(), 0, sizeof(Scal), c->st));
+  LAUNCH(c, launch_filter_sums(g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), c->cnt(), c->st));
+  // z-chunking of the operator grid: minimise waves x planes per block
+  const dim3 og = op_grid(g, 1);
+  const long long tiles = (long long)og.x * og.y;
+  int occ = tomo::op_occupancy(OP_PCG);
+  if (occ < 1) occ = 1;
+  const long long slots = (long long)occ * c->sms;
+  double best = 1e300;
+  int bestc = 1;
+  const int cmax = std::min(g.nnz, 64);
+  for (int ch = 1; ch <= cmax; ++ch) {
+    if ((size_t)tiles * ch > c->n_part / 2) break;
+    const long long waves = (tiles * ch + slots - 1) / slots;
+    const double planes = std::ceil((double)g.nnz / ch) + 2.0;
+    const double cost = waves * planes;
+    if (cost < best - 1e-9) { best = cost; bestc = ch; }
+  }
+  c->nchunk = bestc;
+  c->opg = op_grid(g, bestc);
+  c->nb_b = (int)std::min<long long>((g.ndof + 255) / 256, (long long)c->sms * 4);
+  c->nb_s = (int)std::min<long long>((g.ne + 255) / 256, (long long)c->sms * 8);
+  c->nb_oc = std::min(oc_max_blocks(), (int)std::max<long long>(1, (g.ne + 255) / 256));
+  if ((size_t)c->nb_oc * 2 > c->n_part) c->nb_oc = (int)(c->n_part / 2);
+  CK(c, cudaStreamSynchronize(c->st));
+  c->bound = true;
+  return TOMO_OK;
+}
+
+// ====================================================================== helpers
+namespace {
+
+int need_bound(tomo_ctx* c) {
+  if (!c) return TOMO_EINVAL;
+  if (!c->bound) return fail(c, TOMO_ENOWORKSPACE, "call tomo_bind first");
+  return TOMO_OK;
+}
+
+// E = SIMP(rho) and D^-1 into the workspace; checks rho in [0,1]
+int prepare_modulus(tomo_ctx* c, const double* d_rho, bool jacobi) {
+  const Grid& g = c->g;
+  CK(c, cudaMemsetAsync(&c->scal()->domain_bad, 0, sizeof(int), c->st));
+  LAUNCH(c, launch_simp(g, d_rho, c->E(), c->E0, c->Emin, c->penal, c->scal(), c->st));
+  if (jacobi) LAUNCH(c, launch_jacobi(g, c->E(), c->ke_diag, c->dinv(), c->st));
+  int badv = 0;
+  CK(c, cudaMemcpyAsync(&badv, &c->scal()->domain_bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  if (badv) return fail(c, TOMO_EDOMAIN, "density outside [0,1] (SPEC.md l.118)");
+  return TOMO_OK;
+}
+
+OpArgs op_args(tomo_ctx* c) {
+  OpArgs a{};
+  a.g = c->g;
+  a.w = c->w;
+  a.E = c->E();
+  a.mask = c->dmask();
+  a.dinv = c->dinv();
+  a.partials = c->part();
+  a.s = c->scal();
+  a.nchunk = c->nchunk;
+  return a;
+}
+
+int apply_internal(tomo_ctx* c, const double* d_u, double* d_y) {
+  OpArgs a = op_args(c);
+  a.in = d_u;
+  a.out = d_y;
+  LAUNCH(c, launch_op(OP_APPLY, a, c->opg, c->st));
+  return TOMO_OK;
+}
+
+// PCG on the bound workspace: E / dinv ready; c->u() holds x0 (masked). Returns iterations.
+int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) {
+  const Grid& g = c->g;
+  Scal hs{};
+  LAUNCH(c, launch_scal_init(c->scal(), tol * c->fnorm, max_iters, c->st));
+  // r0 = f - K u0 ; rr0, rz0
+  int rc = apply_internal(c, c->u(), c->q());
+  if (rc) return rc;
+  LAUNCH(c, launch_resid(g, c->q(), c->r(), c->ld(), c->lv(), (int)c->load_dofs.size(), c->st));
+  LAUNCH(c, launch_pcg_b(g, c->r(), c->q(), c->dinv(), c->scal(), c->part(), c->nb_b, 0, c->st));
+  CK(c, cudaMemsetAsync(c->p(0), 0, sizeof(double) * (size_t)g.ndof, c->st));
+  OpArgs a = op_args(c);
+  a.in = c->r();
+  a.u = c->u();
+  a.out = c->q();
+  int k = 0;  // iterations launched
+  int batch = 8;
+  const bool prof = c->prof;
+  if (prof) {
+    const size_t need = 4 * 256;
+    while (c->ev.size() < need) {
+      cudaEvent_t e;
+      CK(c, cudaEventCreate(&e));
+      c->ev.push_back(e);
+    }
+  }
+  for (;;) {
+    CK(c, cudaMemcpyAsync(&hs, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
+    CK(c, cudaStreamSynchronize(c->st));
+    if (hs.done || k >= max_iters) break;
+    const int nb = std::min(batch, max_iters - k);
+    for (int i = 0; i < nb; ++i) {
+      const int it = k + i + 1;  // 1-based iteration
+      a.pold = c->p((it - 1) & 1);
+      a.pnew = c->p(it & 1);
+      if (prof && i < 256) CK(c, cudaEventRecord(c->ev[4 * i], c->st));
+      LAUNCH(c, launch_op(OP_PCG, a, c->opg, c->st));
+      if (prof && i < 256) CK(c, cudaEventRecord(c->ev[4 * i + 1], c->st));
+      LAUNCH(c, launch_pcg_b(g, c->r(), c->q(), c->dinv(), c->scal(), c->part(), c->nb_b, 1, c->st));
+      if (prof && i < 256) CK(c, cudaEventRecord(c->ev[4 * i + 2], c->st));
+    }
+    const int iters_before = hs.iters;
+    k += nb;
+    if (prof) {
+      Scal h2{};
+      CK(c, cudaMemcpyAsync(&h2, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
+      CK(c, cudaStreamSynchronize(c->st));
+      const int real = std::min(h2.iters - iters_before, std::min(nb, 256));
+      for (int i = 0; i < real; ++i) {
+        float ta = 0, tb = 0;
+        CK(c, cudaEventElapsedTime(&ta, c->ev[4 * i], c->ev[4 * i + 1]));
+        CK(c, cudaEventElapsedTime(&tb, c->ev[4 * i + 1], c->ev[4 * i + 2]));
+        c->prof_a_ms += ta;
+        c->prof_b_ms += tb;
+        ++c->prof_n;
+      }
+    }
+    if (batch < 128) batch *= 2;
+  }
+  if (hs.done == 3) {
+    return fail(c, hs.status ? hs.status : TOMO_EBREAKDOWN,
+                hs.status == TOMO_ENAN ? "NaN/Inf in PCG" : "PCG breakdown: p^T K p <= 0 (SPEC.md l.173)");
+  }
+  LAUNCH(c, launch_finish(g, c->u(), c->p(0), c->p(1), c->dmask(), c->scal(), c->st));
+  // true residual
+  rc = apply_internal(c, c->u(), c->q());
+  if (rc) return rc;
+  LAUNCH(c, launch_resid(g, c->q(), c->p(0), c->ld(), c->lv(), (int)c->load_dofs.size(), c->st));
+  LAUNCH(c, launch_pcg_b(g, c->p(0), c->q(), c->dinv(), c->scal(), c->part(), c->nb_b, 2, c->st));
+  CK(c, cudaMemcpyAsync(&hs, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  if (info) {
+    info->iterations = hs.iters;
+    info->converged = hs.done == 1;
+    info->rel_res_recursive = c->fnorm > 0 ? std::sqrt(hs.rr) / c->fnorm : 0.0;
+    info->rel_res_true = c->fnorm > 0 ? std::sqrt(hs.rr_true) / c->fnorm : 0.0;
+  }
+  return hs.iters;
+}
+
+}  // namespace
+
+// ====================================================================== operator / solve
+extern "C" int tomo_apply(tomo_ctx* c, const double* d_rho, int64_t n_e, const double* d_u,
+                          double* d_y, int64_t n_dof) {
+  if (int rc = need_bound(c)) return rc;
+  if (n_e != c->g.ne || n_dof != c->g.ndof) return fail(c, TOMO_ESIZE, "length mismatch (SPEC.md l.127)");
+  if (!check_ptr(d_rho) || !check_ptr(d_u) || !check_ptr(d_y)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  if (d_u == d_y) return fail(c, TOMO_EINVAL, "u and y must not alias");
+  if (int rc = prepare_modulus(c, d_rho, false)) return rc;
+  return apply_internal(c, d_u, d_y);
+}
+
+extern "C" int tomo_solve(tomo_ctx* c, const double* d_rho, int64_t n_e, double* d_u,
+                          int64_t n_dof, double tol, int max_iters, tomo_solve_info* info) {
+  if (int rc = need_bound(c)) return rc;
+  if (n_e != c->g.ne || n_dof != c->g.ndof) return fail(c, TOMO_ESIZE, "length mismatch (SPEC.md l.127)");
+  if (!check_ptr(d_rho) || !check_ptr(d_u)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  if (!(tol >= 0) || max_iters < 0) return fail(c, TOMO_EINVAL, "bad tol / max_iters");
+  if (c->fnorm == 0.0) {  // f = 0: u = 0, no iterations
+    CK(c, cudaMemsetAsync(d_u, 0, sizeof(double) * (size_t)n_dof, c->st));
+    CK(c, cudaStreamSynchronize(c->st));
+    if (info) *info = tomo_solve_info{0, 1, 0.0, 0.0};
+    return 0;
+  }
+  if (int rc = prepare_modulus(c, d_rho, true)) return rc;
+  LAUNCH(c, launch_copy_masked(c->g, d_u, c->u(), c->dmask(), c->st));
+  const int it = pcg_internal(c, tol, max_iters, info);
+  if (it < 0) return it;
+  CK(c, cudaMemcpyAsync(d_u, c->u(), sizeof(double) * (size_t)n_dof, cudaMemcpyDeviceToDevice, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return it;
+}
+
+extern "C" int tomo_compliance(tomo_ctx* c, const double* d_u, int64_t n_dof, double* c_out) {
+  if (int rc = need_bound(c)) return rc;
+  if (n_dof != c->g.ndof) return fail(c, TOMO_ESIZE, "length mismatch");
+  if (!check_ptr(d_u) || !c_out) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  LAUNCH(c, launch_compliance(d_u, c->ld(), c->lv(), (int)c->load_dofs.size(), c->scal(), c->st));
+  CK(c, cudaMemcpyAsync(c_out, &c->scal()->comp, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return TOMO_OK;
+}
+
+extern "C" int tomo_sensitivity(tomo_ctx* c, const double* d_rho, const double* d_u,
+                                double* d_dc, double* d_ce, double* energy_out) {
+  if (int rc = need_bound(c)) return rc;
+  if (!check_ptr(d_rho) || !check_ptr(d_u) || !check_ptr(d_dc) || (d_ce && !check_ptr(d_ce)))
+    return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  LAUNCH(c, launch_sens(c->g, c->w, d_rho, d_u, c->dmask(), c->penal, c->E0 - c->Emin, c->Emin,
+                        d_dc, d_ce, c->part(), c->nb_s, c->scal(), energy_out ? 1 : 0, c->st));
+  if (energy_out) {
+    CK(c, cudaMemcpyAsync(energy_out, &c->scal()->energy, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(c, cudaStreamSynchronize(c->st));
+  }
+  return TOMO_OK;
+}
+
+extern "C" int tomo_filter(tomo_ctx* c, const double* d_in, double* d_out, int64_t n_e,
+                           int transpose) {
+  if (int rc = need_bound(c)) return rc;
+  if (n_e != c->g.ne) return fail(c, TOMO_ESIZE, "length mismatch");
+  if (!check_ptr(d_in) || !check_ptr(d_out)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  if (d_in == d_out) return fail(c, TOMO_EINVAL, "in and out must not alias");
+  LAUNCH(c, launch_filter(c->g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), d_in, d_out,
+                          transpose ? 1 : 0, c->st));
+  return TOMO_OK;
+}
+
+extern "C" int tomo_volume_grad(tomo_ctx* c, double* d_dv, int64_t n_e) {
+  if (int rc = need_bound(c)) return rc;
+  if (n_e != c->g.ne) return fail(c, TOMO_ESIZE, "length mismatch");
+  if (!check_ptr(d_dv)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  // ones into t1, then P^T
+  std::vector<double> ones((size_t)n_e, 1.0);
+  CK(c, cudaMemcpyAsync(c->t1(), ones.data(), sizeof(double) * (size_t)n_e, cudaMemcpyHostToDevice, c->st));
+  LAUNCH(c, launch_filter(c->g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), c->t1(), d_dv, 1, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return TOMO_OK;
+}
+
+extern "C" int tomo_oc_update(tomo_ctx* c, const double* d_x, const double* d_g,
+                              const double* d_dv, int64_t n_e, double volfrac, double move,
+                              double eta, double* d_xnew, double* lambda_out, int* steps_out) {
+  if (int rc = need_bound(c)) return rc;
+  if (n_e != c->g.ne) return fail(c, TOMO_ESIZE, "length mismatch");
+  if (!check_ptr(d_x) || !check_ptr(d_g) || !check_ptr(d_dv) || !check_ptr(d_xnew))
+    return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  if (!(volfrac > 0 && volfrac <= 1) || !(move > 0) || !(eta > 0)) return fail(c, TOMO_EINVAL, "bad OC parameters");
+  const double target = volfrac * (double)n_e;
+  CK(c, launch_oc((int)n_e, d_x, d_g, d_dv, d_xnew, target, move, eta, c->part(), c->ocout(), c->nb_oc, c->st));
+  ++c->launches;
+  double o[2];
+  CK(c, cudaMemcpyAsync(o, c->ocout(), sizeof(o), cudaMemcpyDeviceToHost, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  if (std::isnan(o[0])) return fail(c, TOMO_EBRACKET, "NaN in OC bisection (SPEC.md l.322)");
+  if (lambda_out) *lambda_out = o[0];
+  if (steps_out) *steps_out = (int)o[1];
+  return TOMO_OK;
+}
+
+// ====================================================================== evaluation
+namespace {
+int evaluate_dev(tomo_ctx* c, const double* d_rho, double* d_u, double* d_dc, double* d_dcf,
+                 double tol, int max_iters, double* c_out, tomo_solve_info* info) {
+  const int it = tomo_solve(c, d_rho, c->g.ne, d_u, c->g.ndof, tol, max_iters, info);
+  if (it < 0) return it;
+  double* dc = d_dc ? d_dc : c->t0();
+  LAUNCH(c, launch_compliance(d_u, c->ld(), c->lv(), (int)c->load_dofs.size(), c->scal(), c->st));
+  LAUNCH(c, launch_sens(c->g, c->w, d_rho, d_u, c->dmask(), c->penal, c->E0 - c->Emin, c->Emin,
+                        dc, nullptr, c->part(), c->nb_s, c->scal(), 0, c->st));
+  LAUNCH(c, launch_filter(c->g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), dc, d_dcf, 1, c->st));
+  if (c_out) {
+    CK(c, cudaMemcpyAsync(c_out, &c->scal()->comp, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  }
+  CK(c, cudaStreamSynchronize(c->st));
+  return it;
+}
+}  // namespace
+
+extern "C" int tomo_evaluate(tomo_ctx* c, const double* d_rho, double* d_u, double* d_dc,
+                             double* d_dcf, double tol, int max_iters, double* c_out,
+                             tomo_solve_info* info) {
+  if (int rc = need_bound(c)) return rc;
+  if (!check_ptr(d_rho) || !check_ptr(d_u) || !check_ptr(d_dcf) || (d_dc && !check_ptr(d_dc)))
+    return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  return evaluate_dev(c, d_rho, d_u, d_dc, d_dcf, tol, max_iters, c_out, info);
+}
+
+extern "C" int tomo_evaluate_host(tomo_ctx* c, const double* h_rho, double* h_u, double* h_dcf,
+                                  double tol, int max_iters, double* c_out,
+                                  tomo_solve_info* info) {
+  if (int rc = need_bound(c)) return rc;
+  if (!h_rho || !h_dcf) return fail(c, TOMO_EINVAL, "NULL host pointer");
+  const size_t be = sizeof(double) * (size_t)c->g.ne, bd = sizeof(double) * (size_t)c->g.ndof;
+  // staging: rho -> t1, u -> us (x0 = 0), dcf -> Hs-sized t0 is used for dc, so dcf -> q? no:
+  // dcf is written into p1's storage, which is dead after the solve.
+  CK(c, cudaMemcpyAsync(c->t1(), h_rho, be, cudaMemcpyHostToDevice, c->st));
+  CK(c, cudaMemsetAsync(c->us(), 0, bd, c->st));
+  double* dcf = c->p(1);
+  const int it = evaluate_dev(c, c->t1(), c->us(), nullptr, dcf, tol, max_iters, c_out, info);
+  if (it < 0) return it;
+  CK(c, cudaMemcpyAsync(h_dcf, dcf, be, cudaMemcpyDeviceToHost, c->st));
+  if (h_u) CK(c, cudaMemcpyAsync(h_u, c->us(), bd, cudaMemcpyDeviceToHost, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return it;
+}
+
+// ====================================================================== introspection
+extern "C" int tomo_get_ke(const tomo_ctx* c, double* out) {
+  if (!c || !out) return TOMO_EINVAL;
+  std::memcpy(out, c->KE, sizeof(c->KE));
+  return TOMO_OK;
+}
+
+extern "C" int tomo_get_fixed_mask(tomo_ctx* c, uint8_t* d_mask) {
+  if (int rc = need_bound(c)) return rc;
+  if (!d_mask) return fail(c, TOMO_EINVAL, "NULL pointer");
+  LAUNCH(c, launch_mask_dofs(c->g, c->dmask(), d_mask, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return TOMO_OK;
+}
+
+extern "C" int tomo_get_load(const tomo_ctx* c, int64_t* dofs, double* vals, int64_t* n) {
+  if (!c || !n) return TOMO_EINVAL;
+  const int64_t m = (int64_t)c->load_dofs.size();
+  if (dofs && vals) {
+    if (*n < m) return TOMO_ESIZE;
+    std::memcpy(dofs, c->load_dofs.data(), sizeof(int64_t) * m);
+    std::memcpy(vals, c->load_vals.data(), sizeof(double) * m);
+  }
+  *n = m;
+  return TOMO_OK;
+}
+
+extern "C" int tomo_get_filter_taps(const tomo_ctx* c, int* off, double* w, int* n) {
+  if (!c || !n) return TOMO_EINVAL;
+  const int m = (int)c->tap_w.size();
+  if (off && w) {
+    if (*n < m) return TOMO_ESIZE;
+    std::memcpy(off, c->taps.data(), sizeof(int) * 3 * m);
+    std::memcpy(w, c->tap_w.data(), sizeof(double) * m);
+  }
+  *n = m;
+  return TOMO_OK;
+}
+
+extern "C" int tomo_get_element_dofs(tomo_ctx* c, int64_t* d_map) {
+  if (int rc = need_bound(c)) return rc;
+  if (!check_ptr(d_map)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  LAUNCH(c, launch_edofs(c->g, reinterpret_cast<long long*>(d_map), c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return TOMO_OK;
+}
+
+extern "C" int tomo_get_neighbor_counts(tomo_ctx* c, int* d_counts) {
+  if (int rc = need_bound(c)) return rc;
+  if (!d_counts) return fail(c, TOMO_EINVAL, "NULL pointer");
+  CK(c, cudaMemcpyAsync(d_counts, c->cnt(), sizeof(int) * (size_t)c->g.ne, cudaMemcpyDeviceToDevice, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return TOMO_OK;
+}
+
+extern "C" int tomo_get_jacobi(tomo_ctx* c, const double* d_rho, double* d_dinv) {
+  if (int rc = need_bound(c)) return rc;
+  if (!check_ptr(d_rho) || !check_ptr(d_dinv)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  if (int rc = prepare_modulus(c, d_rho, true)) return rc;
+  CK(c, cudaMemcpyAsync(d_dinv, c->dinv(), sizeof(double) * (size_t)c->g.nn, cudaMemcpyDeviceToDevice, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return TOMO_OK;
+}
+
+extern "C" int64_t tomo_launch_count(const tomo_ctx* c) { return c ? c->launches : -1; }
+
+extern "C" int tomo_bench_dfma(tomo_ctx* c, double* gflops_out, double* ms_out) {
+  if (int rc = need_bound(c)) return rc;
+  const int blocks = c->sms * 8, iters = 4096;
+  cudaEvent_t e0, e1;
+  CK(c, cudaEventCreate(&e0));
+  CK(c, cudaEventCreate(&e1));
+  LAUNCH(c, launch_dfma(c->part(), blocks, 64, c->st));  // warm-up
+  CK(c, cudaEventRecord(e0, c->st));
+  LAUNCH(c, launch_dfma(c->part(), blocks, iters, c->st));
+  CK(c, cudaEventRecord(e1, c->st));
+  CK(c, cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(c, cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double flops = 2.0 * 8 * 8 * (double)iters * 256.0 * blocks;
+  if (gflops_out) *gflops_out = flops / (ms * 1e-3) / 1e9;
+  if (ms_out) *ms_out = ms;
+  return TOMO_OK;
+}
+
+extern "C" int tomo_set_profiling(tomo_ctx* c, int on) {
+  if (!c) return TOMO_EINVAL;
+  c->prof = on != 0;
+  c->prof_a_ms = c->prof_b_ms = 0;
+  c->prof_n = 0;
+  return TOMO_OK;
+}
+
+extern "C" int tomo_profile_times(const tomo_ctx* c, double* t) {
+  if (!c || !t) return TOMO_EINVAL;
+  t[0] = c->prof_n ? c->prof_a_ms / c->prof_n : 0.0;
+  t[1] = c->prof_n ? c->prof_b_ms / c->prof_n : 0.0;
+  t[2] = (double)c->prof_n;
+  return TOMO_OK;
+}

@@ -1,0 +1,108 @@
+// Internal declarations shared by the libtomo host code (api.cu) and the kernels
+// (kernels.cu). Not part of the ABI; see include/tomo.h.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tomo {
+
+// Structured grid of nx*ny*nz hexahedra; (nx+1)(ny+1)(nz+1) nodes.
+struct Grid {
+  int nx, ny, nz;     // elements per axis
+  int nnx, nny, nnz;  // nodes per axis
+  long long nn;       // nodes
+  long long ne;       // elements
+  long long ndof;     // 3 * nn
+};
+
+// The E=1 element stiffness KE written in the (unnormalised, +-1) tensor-Walsh basis of
+// corner values: D = T KE T^T / 64 has 45 non-zeros out of 576, described by these seven
+// numbers (derived and checked entry by entry in api.cu: walsh_coefficients()).
+//   normal strains : v_x0 = amb w_x0 + b (w_x0 + w_y1 + w_z2)   (and cyclic)
+//   shear          : v_x1 = v_y0 = g (w_x1 + w_y0)              (and xz, yz)
+//   bilinear modes : v_xy0 = c1 w_xy0 + c2 w_yz2, ...,  v_xy2 = c3 (s + w_xy2), s = w_xy2+w_xz1+w_yz0
+//   trilinear mode : v_xyz_c = c4 w_xyz_c
+struct Walsh {
+  double amb, b, g, c1, c2, c3, c4;
+};
+
+// Device-side scalar state of one PCG solve (read/written only by kernels, except the
+// host reads it back once per batch of iterations).
+struct Scal {
+  double alpha;       // alpha of the latest K_A (also the deferred u update factor)
+  double beta;        // beta for the next K_A
+  double rz;          // r^T D^-1 r of the current residual
+  double rr;          // r^T r of the current residual (recursive)
+  double pq;          // p^T K p of the latest iteration
+  double rr0;         // r0^T r0
+  double rr_true;     // ||f - K u||^2 at exit
+  double tol_fnorm;   // tol * ||f||
+  double energy;      // sum_e E_e ce_e (sensitivity)
+  double comp;        // f^T u
+  int iters;          // completed iterations
+  int done;           // 0 running, 1 converged, 2 max_iters, 3 error
+  int status;         // tomo_status of an error
+  int max_iters;
+  int domain_bad;     // a density outside [0,1] / NaN met by k_simp
+  unsigned cntA, cntB, cntR;  // last-block counters (reset by the last block)
+  int pad;
+};
+
+enum OpMode { OP_APPLY = 0, OP_PCG = 1 };
+
+struct OpArgs {
+  Grid g;
+  Walsh w;
+  const double* E;       // N_e
+  const uint8_t* mask;   // N_n, bit c = DOF 3n+c fixed
+  const double* in;      // APPLY: u ; PCG: r
+  const double* pold;    // PCG: p_{k-1}
+  double* pnew;          // PCG: p_k (owned nodes written)
+  double* u;             // PCG: u (owned nodes: u += alpha_{k-1} p_{k-1})
+  const double* dinv;    // PCG: Jacobi, N_n
+  double* out;           // APPLY: y ; PCG: q
+  double* partials;      // PCG: one per block
+  Scal* s;               // PCG
+  int nchunk;            // z chunks (gridDim.z)
+};
+
+// launch helpers (kernels.cu). All enqueue on `st`; return cudaGetLastError().
+constexpr int OP_BY = 8;  // threads per block = 32 * OP_BY
+dim3 op_grid(const Grid& g, int nchunk);
+cudaError_t launch_op(int mode, const OpArgs& a, dim3 grid, cudaStream_t st);
+cudaError_t launch_simp(const Grid& g, const double* rho, double* E, double E0, double Emin,
+                        double penal, Scal* s, cudaStream_t st);
+cudaError_t launch_jacobi(const Grid& g, const double* E, double ke_diag, double* dinv,
+                          cudaStream_t st);
+cudaError_t launch_copy_masked(const Grid& g, const double* src, double* dst,
+                               const uint8_t* mask, cudaStream_t st);
+cudaError_t launch_scal_init(Scal* s, double tol_fnorm, int max_iters, cudaStream_t st);
+// r = -q + f (sparse f), then rr / rz reductions (mode 0: init, 2: true residual)
+cudaError_t launch_resid(const Grid& g, const double* q, double* r, const int64_t* ldofs,
+                         const double* lvals, int nloads, cudaStream_t st);
+cudaError_t launch_pcg_b(const Grid& g, double* r, const double* q, const double* dinv,
+                         Scal* s, double* partials, int nblocks, int mode, cudaStream_t st);
+cudaError_t launch_finish(const Grid& g, double* u, const double* p0, const double* p1,
+                          const uint8_t* mask, Scal* s, cudaStream_t st);
+cudaError_t launch_compliance(const double* u, const int64_t* ldofs, const double* lvals,
+                              int nloads, Scal* s, cudaStream_t st);
+cudaError_t launch_sens(const Grid& g, const Walsh& w, const double* rho, const double* u,
+                        const uint8_t* mask, double penal, double dE, double Emin,
+                        double* dc, double* ce, double* partials, int nblocks, Scal* s,
+                        int want_energy, cudaStream_t st);
+cudaError_t launch_filter_sums(const Grid& g, const int* taps, const double* w, int ntaps,
+                               double* Hs, int* counts, cudaStream_t st);
+cudaError_t launch_filter(const Grid& g, const int* taps, const double* w, int ntaps,
+                          const double* Hs, const double* in, double* out, int transpose,
+                          cudaStream_t st);
+cudaError_t launch_oc(int ne, const double* x, const double* g, const double* dv,
+                      double* xnew, double target, double move, double eta,
+                      double* partials, double* out2, int grid_blocks, cudaStream_t st);
+int oc_max_blocks();
+cudaError_t launch_edofs(const Grid& g, long long* map, cudaStream_t st);
+cudaError_t launch_mask_dofs(const Grid& g, const uint8_t* mask, uint8_t* out,
+                             cudaStream_t st);
+cudaError_t launch_dfma(double* out, int blocks, int iters, cudaStream_t st);
+cudaError_t launch_zero(double* p, long long n, cudaStream_t st);
+
+}  // namespace tomo
