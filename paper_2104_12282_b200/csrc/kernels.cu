@@ -269,9 +269,11 @@ __global__ void __launch_bounds__(NT, 2) k_op(const OpArgs a) {
       }
       if (v) mreg |= ((unsigned)(__ldg(a.mask + node) >> sl_c[s]) & 1u) << s;
     }
-    // modulus of element plane kn (used by the next step, which computes element kn)
-    const bool ev = colv && kn >= 0 && kn < g.nz;
-    cp_async8(&STE[t], a.E + (ev ? ecol + plane_e * kn : 0), ev);
+    // modulus of element plane kn-1, the element between node planes kn-1 and kn (computed
+    // in the step that consumes this staging)
+    const int ke = kn - 1;
+    const bool ev = colv && ke >= 0 && ke < g.nz;
+    cp_async8(&STE[t], a.E + (ev ? ecol + plane_e * ke : 0), ev);
     cp_async_commit();
   };
 

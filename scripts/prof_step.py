@@ -1,0 +1,20 @@
+"""Short profiling driver: a few fused PCG iterations (K_A + K_B) at a BASELINE config, for ncu.
+   python scripts/prof_step.py [cfg] [iters]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2104_12282_b200 import inputs, tomo  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+p = inputs.CONFIGS[cfg]
+t = tomo.Tomo(tomo.params_from_problem(p), device="cuda:0")
+rho = torch.tensor(inputs.density_for(cfg), dtype=torch.float64, device="cuda:0")
+u, info = t.solve(rho, tol=1e-10, max_iters=iters)
+dc = t.sensitivity(rho, u)
+dcf = t.filter(dc, transpose=True)
+torch.cuda.synchronize()
+print("ok", cfg, info.as_dict())

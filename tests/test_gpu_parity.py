@@ -144,8 +144,10 @@ def test_cfg0_gradient_parity(cfg0):
     assert rel(cpu(dc), dc_ref) <= 1e-8
     assert rel(cpu(dcf), dcf_ref) <= 1e-8
     # operator-level parity of the sensitivity on the same u (no solver noise)
+    # (Walsh-basis w^T D w vs the oracle's dense u^T KE u: different summation order, so
+    # rounding-level only)
     dc_same, _ = op.sensitivity(rho, cpu(u_g))
-    assert rel(cpu(dc), dc_same) <= 1e-13
+    assert rel(cpu(dc), dc_same) <= 1e-12
     # energy identity u^T K u = f^T u at convergence from x0 = 0 (App. A-6)
     assert abs(energy - c) / c <= 1e-9
 
