@@ -2,8 +2,12 @@
 //
 // Host-only work at tomo_create (KE by quadrature and its Walsh-basis core, BC mask and
 // load list, filter taps); device work is enqueued on the stream bound by tomo_bind into
-// the caller's workspace. The PCG driver launches the fused K_A / K_B kernel pair per
+// the caller's workspace. tomo_bind also encodes the TMA tensor maps of the internal
+// (padded) PCG vectors. The PCG driver launches the fused K_A / K_B kernel pair per
 // iteration (kernels.cu) and reads the device scalars back once per batch of iterations.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -16,18 +20,15 @@
 
 using namespace tomo;
 
-namespace tomo {
-int op_occupancy(int mode);
-}
-
 struct tomo_ctx {
   Grid g{};
   double h = 1, E0 = 1, Emin = 1e-9, nu = 0.3, penal = 3, rmin = 1.5;
   double KE[576];
   Walsh w{};
   double ke_diag = 0;
-  std::vector<uint8_t> mask;       // per node, bit c = DOF 3n+c fixed
-  std::vector<int64_t> load_dofs;  // distinct, ascending insertion order
+  std::vector<uint8_t> mask;       // dense per node, bit c = DOF 3n+c fixed
+  std::vector<int64_t> load_dofs;  // dense DOF indices, distinct, insertion order
+  std::vector<int64_t> load_dofs_pad;
   std::vector<double> load_vals;
   double fnorm = 0;
   std::vector<int> taps;  // 3 per tap
@@ -38,14 +39,17 @@ struct tomo_ctx {
   cudaStream_t st = nullptr;
   char* ws = nullptr;
   size_t ws_bytes = 0;
-  size_t off_E, off_dinv, off_Hs, off_t0, off_t1, off_u, off_r, off_p0, off_p1, off_q, off_us,
-      off_mask, off_cnt, off_ld, off_lv, off_taps, off_tw, off_part, off_scal, off_oc, off_end;
+  size_t off_E, off_dinv, off_Hs, off_t0, off_t1, off_t2, off_u, off_r, off_p0, off_p1, off_q, off_us,
+      off_mask, off_cnt, off_ld, off_ldp, off_lv, off_taps, off_tw, off_part, off_scal, off_oc,
+      off_end;
   size_t n_part = 0;
   int nchunk = 1;
   dim3 opg;
   int nb_b = 1, nb_s = 1, nb_oc = 1;
   int64_t launches = 0;
   int sms = 148;
+  // operator launch variants (tensor maps bound to workspace buffers)
+  OpArgs op_apply_u{}, op_apply_p0{}, op_pcg_odd{}, op_pcg_even{};
   // profiling
   bool prof = false;
   double prof_a_ms = 0, prof_b_ms = 0;
@@ -59,6 +63,7 @@ struct tomo_ctx {
   double* Hs() const { return P<double>(off_Hs); }
   double* t0() const { return P<double>(off_t0); }
   double* t1() const { return P<double>(off_t1); }
+  double* t2() const { return P<double>(off_t2); }
   double* u() const { return P<double>(off_u); }
   double* r() const { return P<double>(off_r); }
   double* p(int i) const { return P<double>(i ? off_p1 : off_p0); }
@@ -67,6 +72,7 @@ struct tomo_ctx {
   uint8_t* dmask() const { return P<uint8_t>(off_mask); }
   int* cnt() const { return P<int>(off_cnt); }
   int64_t* ld() const { return P<int64_t>(off_ld); }
+  int64_t* ldp() const { return P<int64_t>(off_ldp); }
   double* lv() const { return P<double>(off_lv); }
   int* dtaps() const { return P<int>(off_taps); }
   double* tw() const { return P<double>(off_tw); }
@@ -86,16 +92,16 @@ int cuda_fail(tomo_ctx* c, cudaError_t e, const char* where) {
   return fail(c, TOMO_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-#define CK(ctx, expr)                                     \
-  do {                                                    \
-    cudaError_t _e = (expr);                              \
+#define CK(ctx, expr)                                        \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
     if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr); \
   } while (0)
 
-#define LAUNCH(ctx, expr)  \
-  do {                     \
-    CK(ctx, (expr));       \
-    ++(ctx)->launches;     \
+#define LAUNCH(ctx, expr) \
+  do {                    \
+    CK(ctx, (expr));      \
+    ++(ctx)->launches;    \
   } while (0)
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -226,6 +232,37 @@ inline long long node_id(const Grid& g, int i, int j, int k) {
 
 bool check_ptr(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 7) == 0; }
 
+// ---------------------------------------------------------------- TMA tensor maps
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D tiled map over a [d2][d1][d0] array with byte pitches pitch1 (row) and pitch2 (plane)
+int make_map(tomo_ctx* c, CUtensorMap* tm, CUtensorMapDataType dt, void* base, uint64_t d0,
+             uint64_t d1, uint64_t d2, uint64_t pitch1, uint64_t pitch2, uint32_t b0,
+             uint32_t b1) {
+  auto fn = encode_fn();
+  if (!fn) return fail(c, TOMO_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {pitch1, pitch2};
+  const cuuint32_t box[3] = {b0, b1, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(tm, dt, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, TOMO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return TOMO_OK;
+}
+
 }  // namespace
 
 // ====================================================================== lifetime
@@ -249,10 +286,17 @@ extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, doubl
   Grid& g = c->g;
   g.nx = gr->nelx; g.ny = gr->nely; g.nz = gr->nelz;
   g.nnx = g.nx + 1; g.nny = g.ny + 1; g.nnz = g.nz + 1;
+  g.nnx_pad = g.nnx + (g.nnx & 1);
+  g.nx_pad = g.nx + (g.nx & 1);
+  g.mp = (g.nnx + 15) & ~15;
   g.nn = (long long)g.nnx * g.nny * g.nnz;
   g.ne = (long long)g.nx * g.ny * g.nz;
   g.ndof = 3 * g.nn;
-  if (g.ndof >= (1LL << 40)) return bad("grid too large");
+  g.nn_pad = (long long)g.nnx_pad * g.nny * g.nnz;
+  g.ne_pad = (long long)g.nx_pad * g.ny * g.nz;
+  g.ndof_pad = 3 * g.nn_pad;
+  g.mask_bytes = (long long)g.mp * g.nny * g.nnz;
+  if (g.ndof_pad >= (1LL << 31) - 64) return bad("grid too large (internal DOF index is 32-bit)");
   c->h = gr->h; c->E0 = E0; c->Emin = Emin; c->nu = nu; c->penal = penal; c->rmin = rmin;
   build_ke(nu, gr->h, c->KE);
   double dev = 0;
@@ -301,6 +345,11 @@ extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, doubl
       if (c->load_dofs[i] == l.first) { c->load_vals[i] += l.second; merged = true; break; }
     if (!merged) { c->load_dofs.push_back(l.first); c->load_vals.push_back(l.second); }
   }
+  for (int64_t d : c->load_dofs) {
+    const long long n = d / 3;
+    const int i = (int)(n % g.nnx), j = (int)((n / g.nnx) % g.nny), k = (int)(n / ((long long)g.nnx * g.nny));
+    c->load_dofs_pad.push_back(3 * node_pad(g, i, j, k) + d % 3);
+  }
   double ff = 0;
   for (double v : c->load_vals) ff += v * v;
   c->fnorm = std::sqrt(ff);
@@ -320,21 +369,23 @@ extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, doubl
   // workspace layout
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
-  const size_t vd = sizeof(double) * (size_t)g.ndof, ve = sizeof(double) * (size_t)g.ne;
-  c->off_E = take(ve);
-  c->off_dinv = take(sizeof(double) * (size_t)g.nn);
+  const size_t vp = sizeof(double) * (size_t)g.ndof_pad, ve = sizeof(double) * (size_t)g.ne;
+  c->off_E = take(sizeof(double) * (size_t)g.ne_pad);
+  c->off_dinv = take(sizeof(double) * (size_t)g.nn_pad);
   c->off_Hs = take(ve);
   c->off_t0 = take(ve);
   c->off_t1 = take(ve);
-  c->off_u = take(vd);
-  c->off_r = take(vd);
-  c->off_p0 = take(vd);
-  c->off_p1 = take(vd);
-  c->off_q = take(vd);
-  c->off_us = take(vd);
-  c->off_mask = take((size_t)g.nn);
+  c->off_t2 = take(ve);
+  c->off_u = take(vp);
+  c->off_r = take(vp);
+  c->off_p0 = take(vp);
+  c->off_p1 = take(vp);
+  c->off_q = take(vp);
+  c->off_us = take(sizeof(double) * (size_t)g.ndof);
+  c->off_mask = take((size_t)g.mask_bytes);
   c->off_cnt = take(sizeof(int) * (size_t)g.ne);
   c->off_ld = take(sizeof(int64_t) * (c->load_dofs.size() + 1));
+  c->off_ldp = take(sizeof(int64_t) * (c->load_dofs.size() + 1));
   c->off_lv = take(sizeof(double) * (c->load_dofs.size() + 1));
   c->off_taps = take(sizeof(int) * (c->taps.size() + 3));
   c->off_tw = take(sizeof(double) * (c->tap_w.size() + 1));
@@ -368,6 +419,59 @@ extern "C" int tomo_sizes(const tomo_ctx* c, int64_t out[5]) {
   return TOMO_OK;
 }
 
+namespace {
+// operator launch variants: maps over the padded internal vectors
+int build_op_args(tomo_ctx* c) {
+  const Grid& g = c->g;
+  const uint64_t rowv = 24ull * g.nnx_pad, planev = rowv * g.nny;
+  const uint64_t rown = 8ull * g.nnx_pad, planen = rown * g.nny;
+  const uint64_t rowm = (uint64_t)g.mp, planem = rowm * g.nny;
+  const uint64_t rowe = 8ull * g.nx_pad, planee = rowe * g.ny;
+  const CUtensorMapDataType F64 = CU_TENSOR_MAP_DATA_TYPE_FLOAT64, U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  const uint32_t inw = 3 * (OP_OX + 2) + 2, inh = OP_BY + 1;  // boxes widened: aligned starts
+  CUtensorMap tm_u, tm_uown, tm_r, tm_p0, tm_p1, tm_dinv, tm_mask, tm_E;
+  int rc;
+  auto vec = [&](CUtensorMap* tm, double* base, uint32_t b0, uint32_t b1) {
+    return make_map(c, tm, F64, base, 3ull * g.nnx, g.nny, g.nnz, rowv, planev, b0, b1);
+  };
+  if ((rc = vec(&tm_u, c->u(), inw, inh))) return rc;
+  if ((rc = vec(&tm_uown, c->u(), 3 * OP_OX, OP_OY))) return rc;
+  if ((rc = vec(&tm_r, c->r(), inw, inh))) return rc;
+  if ((rc = vec(&tm_p0, c->p(0), inw, inh))) return rc;
+  if ((rc = vec(&tm_p1, c->p(1), inw, inh))) return rc;
+  if ((rc = make_map(c, &tm_dinv, F64, c->dinv(), g.nnx, g.nny, g.nnz, rown, planen, OP_OX + 4, inh))) return rc;
+  if ((rc = make_map(c, &tm_mask, U8, c->dmask(), g.nnx, g.nny, g.nnz, rowm, planem, 48, inh))) return rc;
+  if ((rc = make_map(c, &tm_E, F64, c->E(), g.nx, g.ny, g.nz, rowe, planee, 32, OP_BY))) return rc;
+  OpArgs base{};
+  base.tm_uown = tm_uown;
+  base.tm_dinv = tm_dinv;
+  base.tm_mask = tm_mask;
+  base.tm_E = tm_E;
+  base.g = g;
+  base.w = c->w;
+  base.partials = c->part();
+  base.s = c->scal();
+  base.nchunk = c->nchunk;
+  c->op_apply_u = base;
+  c->op_apply_u.tm_in = tm_u;
+  c->op_apply_u.out = c->q();
+  c->op_apply_p0 = base;
+  c->op_apply_p0.tm_in = tm_p0;
+  c->op_apply_p0.out = c->q();
+  // iteration k (1-based): p_old = p[(k-1)&1], p_new = p[k&1]
+  c->op_pcg_odd = base;
+  c->op_pcg_odd.tm_in = tm_r;
+  c->op_pcg_odd.tm_pold = tm_p0;
+  c->op_pcg_odd.pnew = c->p(1);
+  c->op_pcg_odd.u = c->u();
+  c->op_pcg_odd.out = c->q();
+  c->op_pcg_even = c->op_pcg_odd;
+  c->op_pcg_even.tm_pold = tm_p1;
+  c->op_pcg_even.pnew = c->p(0);
+  return TOMO_OK;
+}
+}  // namespace
+
 extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   if (!c) return TOMO_EINVAL;
   if (!d_ws || (reinterpret_cast<uintptr_t>(d_ws) & 255)) return fail(c, TOMO_EINVAL, "workspace must be 256-B aligned");
@@ -379,21 +483,27 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   int dev = 0;
   CK(c, cudaGetDevice(&dev));
   CK(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
-  CK(c, cudaMemcpyAsync(c->dmask(), c->mask.data(), (size_t)g.nn, cudaMemcpyHostToDevice, c->st));
+  // zero everything once: pad entries of the internal vectors must read as 0
+  CK(c, cudaMemsetAsync(c->ws, 0, c->off_end, c->st));
+  std::vector<uint8_t> mpad((size_t)g.mask_bytes, 0);
+  for (int k = 0; k < g.nnz; ++k)
+    for (int j = 0; j < g.nny; ++j)
+      for (int i = 0; i < g.nnx; ++i) mpad[mask_index(g, i, j, k)] = c->mask[node_id(g, i, j, k)];
+  CK(c, cudaMemcpyAsync(c->dmask(), mpad.data(), mpad.size(), cudaMemcpyHostToDevice, c->st));
   if (!c->load_dofs.empty()) {
     CK(c, cudaMemcpyAsync(c->ld(), c->load_dofs.data(), sizeof(int64_t) * c->load_dofs.size(), cudaMemcpyHostToDevice, c->st));
+    CK(c, cudaMemcpyAsync(c->ldp(), c->load_dofs_pad.data(), sizeof(int64_t) * c->load_dofs.size(), cudaMemcpyHostToDevice, c->st));
     CK(c, cudaMemcpyAsync(c->lv(), c->load_vals.data(), sizeof(double) * c->load_vals.size(), cudaMemcpyHostToDevice, c->st));
   }
   if (!c->tap_w.empty()) {
     CK(c, cudaMemcpyAsync(c->dtaps(), c->taps.data(), sizeof(int) * c->taps.size(), cudaMemcpyHostToDevice, c->st));
     CK(c, cudaMemcpyAsync(c->tw(), c->tap_w.data(), sizeof(double) * c->tap_w.size(), cudaMemcpyHostToDevice, c->st));
   }
-  CK(c, cudaMemsetAsync(c->scal(), 0, sizeof(Scal), c->st));
   LAUNCH(c, launch_filter_sums(g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), c->cnt(), c->st));
   // z-chunking of the operator grid: minimise waves x planes per block
   const dim3 og = op_grid(g, 1);
   const long long tiles = (long long)og.x * og.y;
-  int occ = tomo::op_occupancy(OP_PCG);
+  int occ = op_occupancy(OP_PCG);
   if (occ < 1) occ = 1;
   const long long slots = (long long)occ * c->sms;
   double best = 1e300;
@@ -408,10 +518,11 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   }
   c->nchunk = bestc;
   c->opg = op_grid(g, bestc);
-  c->nb_b = (int)std::min<long long>((g.ndof + 255) / 256, (long long)c->sms * 4);
+  c->nb_b = (int)std::min<long long>((g.ndof_pad / 2 + 511) / 512, (long long)c->sms * 8);
   c->nb_s = (int)std::min<long long>((g.ne + 255) / 256, (long long)c->sms * 8);
   c->nb_oc = std::min(oc_max_blocks(), (int)std::max<long long>(1, (g.ne + 255) / 256));
   if ((size_t)c->nb_oc * 2 > c->n_part) c->nb_oc = (int)(c->n_part / 2);
+  if (int rc = build_op_args(c)) return rc;
   CK(c, cudaStreamSynchronize(c->st));
   c->bound = true;
   return TOMO_OK;
@@ -439,42 +550,17 @@ int prepare_modulus(tomo_ctx* c, const double* d_rho, bool jacobi) {
   return TOMO_OK;
 }
 
-OpArgs op_args(tomo_ctx* c) {
-  OpArgs a{};
-  a.g = c->g;
-  a.w = c->w;
-  a.E = c->E();
-  a.mask = c->dmask();
-  a.dinv = c->dinv();
-  a.partials = c->part();
-  a.s = c->scal();
-  a.nchunk = c->nchunk;
-  return a;
-}
-
-int apply_internal(tomo_ctx* c, const double* d_u, double* d_y) {
-  OpArgs a = op_args(c);
-  a.in = d_u;
-  a.out = d_y;
-  LAUNCH(c, launch_op(OP_APPLY, a, c->opg, c->st));
-  return TOMO_OK;
-}
-
-// PCG on the bound workspace: E / dinv ready; c->u() holds x0 (masked). Returns iterations.
+// PCG on the bound workspace: E / dinv ready; c->u() holds x0 (padded, masked).
 int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) {
   const Grid& g = c->g;
+  const int nl = (int)c->load_dofs.size();
   Scal hs{};
   LAUNCH(c, launch_scal_init(c->scal(), tol * c->fnorm, max_iters, c->st));
   // r0 = f - K u0 ; rr0, rz0
-  int rc = apply_internal(c, c->u(), c->q());
-  if (rc) return rc;
-  LAUNCH(c, launch_resid(g, c->q(), c->r(), c->ld(), c->lv(), (int)c->load_dofs.size(), c->st));
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->opg, c->st));
+  LAUNCH(c, launch_resid(g, c->q(), c->r(), c->ldp(), c->lv(), nl, c->st));
   LAUNCH(c, launch_pcg_b(g, c->r(), c->q(), c->dinv(), c->scal(), c->part(), c->nb_b, 0, c->st));
-  CK(c, cudaMemsetAsync(c->p(0), 0, sizeof(double) * (size_t)g.ndof, c->st));
-  OpArgs a = op_args(c);
-  a.in = c->r();
-  a.u = c->u();
-  a.out = c->q();
+  CK(c, cudaMemsetAsync(c->p(0), 0, sizeof(double) * (size_t)g.ndof_pad, c->st));
   int k = 0;  // iterations launched
   int batch = 8;
   const bool prof = c->prof;
@@ -493,8 +579,7 @@ int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) 
     const int nb = std::min(batch, max_iters - k);
     for (int i = 0; i < nb; ++i) {
       const int it = k + i + 1;  // 1-based iteration
-      a.pold = c->p((it - 1) & 1);
-      a.pnew = c->p(it & 1);
+      const OpArgs& a = (it & 1) ? c->op_pcg_odd : c->op_pcg_even;
       if (prof && i < 256) CK(c, cudaEventRecord(c->ev[4 * i], c->st));
       LAUNCH(c, launch_op(OP_PCG, a, c->opg, c->st));
       if (prof && i < 256) CK(c, cudaEventRecord(c->ev[4 * i + 1], c->st));
@@ -523,11 +608,10 @@ int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) 
     return fail(c, hs.status ? hs.status : TOMO_EBREAKDOWN,
                 hs.status == TOMO_ENAN ? "NaN/Inf in PCG" : "PCG breakdown: p^T K p <= 0 (SPEC.md l.173)");
   }
-  LAUNCH(c, launch_finish(g, c->u(), c->p(0), c->p(1), c->dmask(), c->scal(), c->st));
-  // true residual
-  rc = apply_internal(c, c->u(), c->q());
-  if (rc) return rc;
-  LAUNCH(c, launch_resid(g, c->q(), c->p(0), c->ld(), c->lv(), (int)c->load_dofs.size(), c->st));
+  LAUNCH(c, launch_finish(g, c->u(), c->p(0), c->p(1), c->scal(), c->st));
+  // true residual ||f - K u||
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->opg, c->st));
+  LAUNCH(c, launch_resid(g, c->q(), c->p(0), c->ldp(), c->lv(), nl, c->st));
   LAUNCH(c, launch_pcg_b(g, c->p(0), c->q(), c->dinv(), c->scal(), c->part(), c->nb_b, 2, c->st));
   CK(c, cudaMemcpyAsync(&hs, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
   CK(c, cudaStreamSynchronize(c->st));
@@ -550,7 +634,10 @@ extern "C" int tomo_apply(tomo_ctx* c, const double* d_rho, int64_t n_e, const d
   if (!check_ptr(d_rho) || !check_ptr(d_u) || !check_ptr(d_y)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
   if (d_u == d_y) return fail(c, TOMO_EINVAL, "u and y must not alias");
   if (int rc = prepare_modulus(c, d_rho, false)) return rc;
-  return apply_internal(c, d_u, d_y);
+  LAUNCH(c, launch_pack(c->g, d_u, c->p(0), nullptr, c->st));
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_p0, c->opg, c->st));
+  LAUNCH(c, launch_unpack(c->g, c->q(), d_y, c->st));
+  return TOMO_OK;
 }
 
 extern "C" int tomo_solve(tomo_ctx* c, const double* d_rho, int64_t n_e, double* d_u,
@@ -566,10 +653,10 @@ extern "C" int tomo_solve(tomo_ctx* c, const double* d_rho, int64_t n_e, double*
     return 0;
   }
   if (int rc = prepare_modulus(c, d_rho, true)) return rc;
-  LAUNCH(c, launch_copy_masked(c->g, d_u, c->u(), c->dmask(), c->st));
+  LAUNCH(c, launch_pack(c->g, d_u, c->u(), c->dmask(), c->st));
   const int it = pcg_internal(c, tol, max_iters, info);
   if (it < 0) return it;
-  CK(c, cudaMemcpyAsync(d_u, c->u(), sizeof(double) * (size_t)n_dof, cudaMemcpyDeviceToDevice, c->st));
+  LAUNCH(c, launch_unpack(c->g, c->u(), d_u, c->st));
   CK(c, cudaStreamSynchronize(c->st));
   return it;
 }
@@ -675,11 +762,10 @@ extern "C" int tomo_evaluate_host(tomo_ctx* c, const double* h_rho, double* h_u,
   if (int rc = need_bound(c)) return rc;
   if (!h_rho || !h_dcf) return fail(c, TOMO_EINVAL, "NULL host pointer");
   const size_t be = sizeof(double) * (size_t)c->g.ne, bd = sizeof(double) * (size_t)c->g.ndof;
-  // staging: rho -> t1, u -> us (x0 = 0), dcf -> Hs-sized t0 is used for dc, so dcf -> q? no:
-  // dcf is written into p1's storage, which is dead after the solve.
+  // staging: rho -> t1, u -> us (x0 = 0), dc -> t0, dcf -> t2
   CK(c, cudaMemcpyAsync(c->t1(), h_rho, be, cudaMemcpyHostToDevice, c->st));
   CK(c, cudaMemsetAsync(c->us(), 0, bd, c->st));
-  double* dcf = c->p(1);
+  double* dcf = c->t2();
   const int it = evaluate_dev(c, c->t1(), c->us(), nullptr, dcf, tol, max_iters, c_out, info);
   if (it < 0) return it;
   CK(c, cudaMemcpyAsync(h_dcf, dcf, be, cudaMemcpyDeviceToHost, c->st));
@@ -747,7 +833,7 @@ extern "C" int tomo_get_jacobi(tomo_ctx* c, const double* d_rho, double* d_dinv)
   if (int rc = need_bound(c)) return rc;
   if (!check_ptr(d_rho) || !check_ptr(d_dinv)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
   if (int rc = prepare_modulus(c, d_rho, true)) return rc;
-  CK(c, cudaMemcpyAsync(d_dinv, c->dinv(), sizeof(double) * (size_t)c->g.nn, cudaMemcpyDeviceToDevice, c->st));
+  LAUNCH(c, launch_dinv_dense(c->g, c->dinv(), d_dinv, c->st));
   CK(c, cudaStreamSynchronize(c->st));
   return TOMO_OK;
 }

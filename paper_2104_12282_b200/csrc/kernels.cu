@@ -9,14 +9,17 @@
 //   k_filter        density filter P / P^T
 //   k_oc            OC update with device bisection
 //
-// Design: KE is never stored. In the tensor-Walsh basis of corner values
-// the 24x24 KE has 45 non-zeros; the operator transforms corner values face by face
-// (2-D Walsh transform of each node plane, shared between the two elements stacked on
-// it), applies the 7-coefficient sparse core scaled by E_e, and transforms back. A block
-// owns a 31x7 column of output nodes and marches along z through a chunk of node
-// planes; inputs are staged with cp.async into per-thread shared-memory slots one plane
-// ahead. All reductions are two-stage and deterministic (fixed partition, fixed-order
-// final sum by the last block); there are no floating-point atomics.
+// Operator design. KE is never stored: in the tensor-Walsh basis of corner
+// values the 24x24 KE has 45 non-zeros. The operator takes the 2-D Walsh transform of every
+// node plane once per element column (shared by the two elements stacked on it), applies
+// the 7-coefficient core scaled by E_e, transforms back, and accumulates the top face of
+// one element with the bottom face of the next in registers. A 32 x 8 block owns a
+// 30 x 7 column of output nodes and marches along z through a chunk of node planes. Every
+// input plane tile (vector incl. halo, Jacobi, mask bytes, E, owned u) is fetched by ONE
+// thread with TMA (cp.async.bulk.tensor, OOB zero fill gives the domain boundary for free)
+// into a 3-stage mbarrier pipeline; outputs are written with coalesced stores.
+// All reductions are two-stage and deterministic (fixed partition, fixed-order final sum
+// by the last block); there are no floating-point atomics.
 #include <cooperative_groups.h>
 
 #include "tomo_internal.h"
@@ -28,25 +31,70 @@ namespace {
 
 constexpr int TX = 32;
 constexpr int BY = OP_BY;
-constexpr int NT = TX * BY;                     // threads per operator block
-constexpr int OUTX = TX - 1;                    // output nodes per tile along x
-constexpr int OUTY = BY - 1;                    // output nodes per tile along y
-constexpr int UROW = 3 * (TX + 1);              // doubles per staged node row (33 nodes)
-constexpr int UPLANE = UROW * (BY + 1);         // doubles per staged node plane
-constexpr int SLOTS = (UPLANE + NT - 1) / NT;   // staged doubles per thread per plane
+constexpr int NT = TX * BY;            // threads per operator block
+constexpr int OX = OP_OX;              // output nodes per tile along x
+constexpr int OY = OP_OY;              // output nodes per tile along y
+constexpr int NS = OP_NS;              // pipeline stages
+constexpr int IN_W = 3 * (OX + 2);     // 96 doubles per input row (32 nodes) in U
+constexpr int IN_H = BY + 1;           // 9 input rows
+constexpr int IN_N = IN_W * IN_H;      // 864
+constexpr int OWN_W = 3 * OX;          // 90 doubles per owned row
+constexpr int OWN_N = OWN_W * OY;      // 630
+// TMA boxes. The innermost box start must be 16-byte aligned (measured on this B200: an
+// 8-byte-aligned start faults with "illegal instruction"), so every box starts at the
+// aligned-down coordinate and is widened; smem reads add the per-block offset.
+constexpr int VB_W = IN_W + 2;         // 98 doubles: vector rows (start offset 0..1)
+constexpr int DB_W = OX + 4;           // 34 doubles: Jacobi rows (start offset 0..1)
+constexpr int MB_W = 48;               // 48 bytes: mask rows (start offset 0..15)
+constexpr int E_W = 32, E_H = BY;      // element box (start offset 0..1, 31 columns used)
+// stage layout in doubles, every piece 128-byte aligned
+constexpr int R_OFF = 0;
+constexpr int PO_OFF = 896;            // 882 used
+constexpr int UO_OFF = 1792;           // 630 used
+constexpr int DI_OFF = 2432;           // 306 used
+constexpr int EE_OFF = 2752;           // 256 used
+constexpr int MK_OFF = 3008;           // 432 bytes used
+constexpr int STAGE = 3072;            // 24576 B
+static_assert(PO_OFF >= VB_W * IN_H && UO_OFF - PO_OFF >= VB_W * IN_H && DI_OFF - UO_OFF >= OWN_N &&
+                  EE_OFF - DI_OFF >= DB_W * IN_H && MK_OFF - EE_OFF >= E_W * E_H &&
+                  (STAGE - MK_OFF) * 8 >= MB_W * IN_H,
+              "stage pieces overlap");
+static_assert((PO_OFF * 8) % 128 == 0 && (UO_OFF * 8) % 128 == 0 && (DI_OFF * 8) % 128 == 0 &&
+                  (EE_OFF * 8) % 128 == 0 && (MK_OFF * 8) % 128 == 0 && (STAGE * 8) % 128 == 0,
+              "TMA destinations must stay 128-byte aligned");
+constexpr unsigned BYTES_PCG = 8u * (2 * VB_W * IN_H + OWN_N + DB_W * IN_H + E_W * E_H) + MB_W * IN_H;
+constexpr unsigned BYTES_APPLY = 8u * (VB_W * IN_H + E_W * E_H) + MB_W * IN_H;
 
-// ------------------------------------------------------------------ small helpers
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int sz = pred ? 8 : 0;  // src-size 0 => zero fill
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz)
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -190,26 +238,54 @@ __device__ __forceinline__ double element_energy(const double (&Flo)[12],
   return e;
 }
 
-// Node index of corner a of element (i,j,k): corner order (0,0,0),(1,0,0),(1,1,0),(0,1,0),
-// (0,0,1),(1,0,1),(1,1,1),(0,1,1). Shared by k_sens and k_edofs.
-__device__ __forceinline__ long long corner_node(const Grid& g, int i, int j, int k, int a) {
-  const int ax = ((a + 1) >> 1) & 1;  // 0,1,1,0
-  const int ay = (a >> 1) & 1;        // 0,0,1,1
-  const int az = a >> 2;
-  return (long long)(i + ax) + (long long)g.nnx * ((j + ay) + (long long)g.nny * (k + az));
+// Corner a of element (i,j,k): order (0,0,0),(1,0,0),(1,1,0),(0,1,0),(0,0,1),(1,0,1),
+// (1,1,1),(0,1,1). Shared by k_sens and k_edofs.
+__device__ __forceinline__ void corner_offset(int a, int& ax, int& ay, int& az) {
+  ax = ((a + 1) >> 1) & 1;  // 0,1,1,0
+  ay = (a >> 1) & 1;        // 0,0,1,1
+  az = a >> 2;
 }
 
 // ------------------------------------------------------------------ operator / K_A
+// box starts (aligned down) of one block's tiles; offsets are the smem shifts
+struct TileOrigin {
+  int xv, xd, xm, xe;  // aligned starts: vector (doubles), Jacobi, mask (bytes), element
+  int ov, od, om, oe;  // offsets of node i0-1 (element i0-1) inside the boxes
+};
+
+__device__ __forceinline__ TileOrigin tile_origin(int i0) {
+  TileOrigin o;
+  const int sv = 3 * (i0 - 1), sn = i0 - 1;
+  o.xv = sv & ~1; o.ov = sv - o.xv;
+  o.xd = sn & ~1; o.od = sn - o.xd;
+  o.xm = sn & ~15; o.om = sn - o.xm;
+  o.xe = sn & ~1; o.oe = sn - o.xe;
+  return o;
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(NT, 2) k_op(const OpArgs a) {
-  constexpr int NARR = (MODE == OP_PCG) ? 4 : 1;
-  extern __shared__ __align__(16) double smem[];
-  double* ST = smem;                          // [SLOTS][NARR][NT] per-thread staging
-  double* STE = ST + SLOTS * NARR * NT;       // [NT] element modulus staging
-  double* U = STE + NT;                       // [UPLANE] current node plane (masked p / u)
-  double* S = U + UPLANE;                     // [9][NT] corner contributions y00,y01,y10
-  double* red = S + 9 * NT;                   // [32]
-  int* s_flag = reinterpret_cast<int*>(red + 32);
+__device__ __forceinline__ void issue_plane(const OpArgs& a, double* stg, uint64_t* bar,
+                                            const TileOrigin& o, int i0, int j0, int kq) {
+  mbar_expect_tx(bar, MODE == OP_PCG ? BYTES_PCG : BYTES_APPLY);
+  tma_load_3d(stg + R_OFF, &a.tm_in, o.xv, j0 - 1, kq, bar);
+  if (MODE == OP_PCG) {
+    tma_load_3d(stg + PO_OFF, &a.tm_pold, o.xv, j0 - 1, kq, bar);
+    tma_load_3d(stg + UO_OFF, &a.tm_uown, 3 * i0, j0, kq, bar);
+    tma_load_3d(stg + DI_OFF, &a.tm_dinv, o.xd, j0 - 1, kq, bar);
+  }
+  tma_load_3d(stg + MK_OFF, &a.tm_mask, o.xm, j0 - 1, kq, bar);
+  tma_load_3d(stg + EE_OFF, &a.tm_E, o.xe, j0 - 1, kq - 1, bar);  // element plane kq-1
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) {
+  extern __shared__ __align__(128) double smem[];
+  double* stages = smem;                     // [NS][STAGE]
+  double* U = stages + NS * STAGE;           // [IN_N] current node plane (masked p / u)
+  double* S = U + IN_N;                      // [9][NT] corner contributions y00,y01,y10
+  double* red = S + 9 * NT;                  // [32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 32);  // [NS]
+  int* s_flag = reinterpret_cast<int*>(bars + NS);
 
   const int tx = threadIdx.x, ty = threadIdx.y, t = ty * TX + tx;
   const Grid& g = a.g;
@@ -221,158 +297,148 @@ __global__ void __launch_bounds__(NT, 2) k_op(const OpArgs a) {
     alpha_prev = *(volatile double*)&a.s->alpha;
   }
 
-  const int i0 = blockIdx.x * OUTX, j0 = blockIdx.y * OUTY;
+  const int i0 = blockIdx.x * OX, j0 = blockIdx.y * OY;
   const int kbeg = (int)(((long long)blockIdx.z * g.nnz) / a.nchunk);
   const int kend = (int)(((long long)(blockIdx.z + 1) * g.nnz) / a.nchunk);
-  const int X = i0 + tx - 1, Y = j0 + ty - 1;
-  const bool colv = X >= 0 && X < g.nx && Y >= 0 && Y < g.ny;
-  const bool outv = tx < OUTX && ty < OUTY && (i0 + tx) <= g.nx && (j0 + ty) <= g.ny;
-  const long long plane_n = (long long)g.nnx * g.nny;
-  const long long plane_e = (long long)g.nx * g.ny;
-  const long long ecol = colv ? (X + (long long)g.nx * Y) : 0;
-  const long long onode_xy = (long long)(i0 + tx) + (long long)g.nnx * (j0 + ty);
+  const int nit = kend - kbeg + 2;
+  const bool colv = tx < OX + 1;  // element column inside the tile (lane 31 idles)
+  const bool outv = tx < OX && ty < OY && (i0 + tx) <= g.nx && (j0 + ty) <= g.ny;
+  const long long rowd = 3LL * g.nnx_pad;
+  const long long planed = rowd * g.nny;
+  const TileOrigin org = tile_origin(i0);
 
-  // static decode of this thread's staging slots (one double of the node plane each)
-  int sl_f[SLOTS], sl_nxy[SLOTS], sl_c[SLOTS];
-  unsigned sl_ok = 0, sl_own = 0;
-#pragma unroll
-  for (int s = 0; s < SLOTS; ++s) {
-    const int f = t + s * NT;
-    const int jj = f / UROW;
-    const int rem = f - jj * UROW;
-    const int ii = rem / 3;
-    const int c = rem - 3 * ii;
-    const int gi = i0 - 1 + ii, gj = j0 - 1 + jj;
-    const bool ok = f < UPLANE && gi >= 0 && gi <= g.nx && gj >= 0 && gj <= g.ny;
-    sl_f[s] = f;
-    sl_nxy[s] = ok ? gi + g.nnx * gj : 0;
-    sl_c[s] = c;
-    if (ok) sl_ok |= 1u << s;
-    if (ok && ii >= 1 && ii <= OUTX && jj >= 1 && jj <= OUTY) sl_own |= 1u << s;
+  if (t == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0) {
+    for (int s = 0; s < NS && s < nit; ++s)
+      issue_plane<MODE>(a, stages + s * STAGE, &bars[s], org, i0, j0, kbeg - 1 + s);
   }
 
-  unsigned mreg = 0;  // bit s: DOF of slot s is fixed
-  auto issue = [&](int kn) {
-    const bool pv = kn >= 0 && kn <= g.nz;
-    const bool pown = kn >= kbeg && kn < kend;
+  double F0[12], F1[12], G0[12], G1[12];
 #pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      if (s * NT + t >= UPLANE) break;
-      const bool v = pv && ((sl_ok >> s) & 1u);
-      const long long node = v ? (long long)sl_nxy[s] + plane_n * kn : 0;
-      const long long d = 3 * node + sl_c[s];
-      cp_async8(&ST[(s * NARR + 0) * NT + t], a.in + d, v);
-      if (MODE == OP_PCG) {
-        cp_async8(&ST[(s * NARR + 1) * NT + t], a.pold + d, v);
-        cp_async8(&ST[(s * NARR + 2) * NT + t], a.dinv + node, v);
-        cp_async8(&ST[(s * NARR + 3) * NT + t], a.u + d, v && pown && ((sl_own >> s) & 1u));
-      }
-      if (v) mreg |= ((unsigned)(__ldg(a.mask + node) >> sl_c[s]) & 1u) << s;
-    }
-    // modulus of element plane kn-1, the element between node planes kn-1 and kn (computed
-    // in the step that consumes this staging)
-    const int ke = kn - 1;
-    const bool ev = colv && ke >= 0 && ke < g.nz;
-    cp_async8(&STE[t], a.E + (ev ? ecol + plane_e * ke : 0), ev);
-    cp_async_commit();
-  };
-
-  double Fcur[12], Gtp[12], pown[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-  for (int i = 0; i < 12; ++i) { Fcur[i] = 0.0; Gtp[i] = 0.0; }
+  for (int i = 0; i < 12; ++i) { F0[i] = 0.0; F1[i] = 0.0; G0[i] = 0.0; G1[i] = 0.0; }
+  double own[3] = {0.0, 0.0, 0.0};  // PCG: p of the own node ; APPLY: raw u of the own node
+  unsigned mown = 0;                // fixed bits of the own node
   double pq = 0.0;
+  const int f_own = (ty + 1) * IN_W + 3 * (tx + 1);                 // in U
+  const int v_own = (ty + 1) * VB_W + org.ov + 3 * (tx + 1);         // in the vector box
+  const int m_own = (ty + 1) * MB_W + org.om + tx + 1;               // in the mask box
 
-  issue(kbeg - 1);
-  const int nit = kend - kbeg + 2;
-  for (int it = 0; it < nit; ++it) {
-    const int kn = kbeg - 1 + it;  // node plane staged in this step
-    cp_async_wait_all();
-    const double Ecur = STE[t];
-    const bool pown_plane = kn >= kbeg && kn < kend;
+  auto body = [&](int it, double (&Fc)[12], double (&Fn)[12], double (&Gp)[12],
+                  double (&Gn)[12]) {
+    const int s = it % NS;
+    double* stg = stages + s * STAGE;
+    const unsigned char* MK = reinterpret_cast<const unsigned char*>(stg + MK_OFF);
+    mbar_wait(&bars[s], (unsigned)(it / NS) & 1u);
+    const int kn = kbeg - 1 + it;  // node plane of this step
+    const bool own_plane = kn >= kbeg && kn < kend;
+    // ---- stage -> U: p = D^-1 r + beta p_old (PCG) or masked u (APPLY)
 #pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      if (s * NT + t >= UPLANE) break;
-      const bool fixed = (mreg >> s) & 1u;
-      double v;
-      if (MODE == OP_PCG) {
-        const double r = ST[(s * NARR + 0) * NT + t];
-        const double po = ST[(s * NARR + 1) * NT + t];
-        const double di = ST[(s * NARR + 2) * NT + t];
-        v = fixed ? 0.0 : fma(di, r, beta * po);
-        if (pown_plane && ((sl_own >> s) & 1u)) {
-          const long long d = 3 * ((long long)sl_nxy[s] + plane_n * kn) + sl_c[s];
-          a.pnew[d] = v;
-          a.u[d] = fma(alpha_prev, po, ST[(s * NARR + 3) * NT + t]);
+    for (int q = 0; q < (IN_N + NT - 1) / NT; ++q) {
+      const int f = t + q * NT;
+      if (f < IN_N) {
+        const int jj = f / IN_W;
+        const int x = f - jj * IN_W;
+        const int ii = x / 3;
+        const int c = x - 3 * ii;
+        const bool fixed = (MK[jj * MB_W + org.om + ii] >> c) & 1u;
+        const int fv = jj * VB_W + org.ov + x;
+        double v;
+        if (MODE == OP_PCG) {
+          const double po = stg[PO_OFF + fv];
+          v = fixed ? 0.0 : fma(stg[DI_OFF + jj * DB_W + org.od + ii], stg[R_OFF + fv], beta * po);
+          if (own_plane && jj >= 1 && jj <= OY && ii >= 1 && ii <= OX) {
+            const int gi = i0 - 1 + ii, gj = j0 - 1 + jj;
+            if (gi <= g.nx && gj <= g.ny) {
+              const long long gidx = 3LL * (i0 - 1) + x + rowd * gj + planed * kn;
+              a.pnew[gidx] = v;
+              a.u[gidx] = fma(alpha_prev, po, stg[UO_OFF + (jj - 1) * OWN_W + (x - 3)]);
+            }
+          }
+        } else {
+          v = fixed ? 0.0 : stg[R_OFF + fv];
         }
-      } else {
-        v = fixed ? 0.0 : ST[(s * NARR + 0) * NT + t];
+        U[f] = v;
       }
-      U[sl_f[s]] = v;
     }
-    mreg = 0;
-    if (it + 1 < nit) issue(kn + 1);
-    __syncthreads();
-
-    double Fnew[12];
-    {
-      const double* r0 = U + ty * UROW + tx * 3;
-      const double* r1 = r0 + UROW;
+    const double Ecur = colv ? stg[EE_OFF + ty * E_W + org.oe + tx] : 0.0;
+    unsigned mown_next = 0;
+    double raw_next[3] = {0.0, 0.0, 0.0};
+    if (tx < OX && ty < OY) {
+      mown_next = MK[m_own];
+      if (MODE == OP_APPLY) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) face_from(r0[c], r0[3 + c], r1[c], r1[3 + c], Fnew, c);
+        for (int c = 0; c < 3; ++c) raw_next[c] = stg[R_OFF + v_own + c];
+      }
     }
-    double pown_next[3];
+    __syncthreads();  // U complete; stage s consumed
+    if (t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
+
+    double y11[3] = {0.0, 0.0, 0.0};
+    if (colv) {
+      const double* r0 = U + ty * IN_W + tx * 3;
+      const double* r1 = r0 + IN_W;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) face_from(r0[c], r0[3 + c], r1[c], r1[3 + c], Fn, c);
+      if (it >= 1) {
+        double Gb[12];
+        element_core(Fc, Fn, Ecur, a.w, Gb, Gn);
+        if (it >= 2) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double m00 = Gp[0 + c] + Gb[0 + c];
+            const double m10 = Gp[3 + c] + Gb[3 + c];
+            const double m01 = Gp[6 + c] + Gb[6 + c];
+            const double m11 = Gp[9 + c] + Gb[9 + c];
+            const double A_ = m00 - m01, B_ = m10 - m11, C_ = m00 + m01, D_ = m10 + m11;
+            S[(0 + c) * NT + t] = A_ - B_;  // y00
+            S[(3 + c) * NT + t] = C_ - D_;  // y01
+            S[(6 + c) * NT + t] = A_ + B_;  // y10
+            y11[c] = C_ + D_;
+          }
+        }
+      }
+    }
+    double own_next[3];
     if (MODE == OP_PCG) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) pown_next[c] = U[(ty + 1) * UROW + (tx + 1) * 3 + c];
-    }
-    double y11[3] = {0.0, 0.0, 0.0};
-    if (it >= 1) {
-      double Gb[12], Gt[12];
-      element_core(Fcur, Fnew, Ecur, a.w, Gb, Gt);
-      if (it >= 2) {
+      for (int c = 0; c < 3; ++c) own_next[c] = (tx < OX && ty < OY) ? U[f_own + c] : 0.0;
+    } else {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double m00 = Gtp[0 + c] + Gb[0 + c];
-          const double m10 = Gtp[3 + c] + Gb[3 + c];
-          const double m01 = Gtp[6 + c] + Gb[6 + c];
-          const double m11 = Gtp[9 + c] + Gb[9 + c];
-          const double A_ = m00 - m01, B_ = m10 - m11, C_ = m00 + m01, D_ = m10 + m11;
-          S[(0 + c) * NT + t] = A_ - B_;  // y00
-          S[(3 + c) * NT + t] = C_ - D_;  // y01
-          S[(6 + c) * NT + t] = A_ + B_;  // y10
-          y11[c] = C_ + D_;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 12; ++i) Gtp[i] = Gt[i];
+      for (int c = 0; c < 3; ++c) own_next[c] = raw_next[c];
     }
-    __syncthreads();
+    __syncthreads();  // S complete
     if (it >= 2 && outv) {
       const int ko = kn - 1;  // output node plane
-      const long long node = onode_xy + plane_n * ko;
-      const unsigned m = __ldg(a.mask + node);
+      const long long gbase = 3LL * (i0 + tx) + rowd * (j0 + ty) + planed * ko;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        double q = y11[c] + S[(3 + c) * NT + t + 1] + S[(6 + c) * NT + t + TX] +
-                   S[(0 + c) * NT + t + TX + 1];
-        const bool fixed = (m >> c) & 1u;
-        const long long d = 3 * node + c;
+        double qv = y11[c] + S[(3 + c) * NT + t + 1] + S[(6 + c) * NT + t + TX] +
+                    S[(0 + c) * NT + t + TX + 1];
+        const bool fixed = (mown >> c) & 1u;
         if (MODE == OP_PCG) {
-          q = fixed ? 0.0 : q;
-          a.out[d] = q;
-          pq = fma(pown[c], q, pq);
+          qv = fixed ? 0.0 : qv;
+          a.out[gbase + c] = qv;
+          pq = fma(own[c], qv, pq);
         } else {
-          a.out[d] = fixed ? a.in[d] : q;
+          a.out[gbase + c] = fixed ? own[c] : qv;
         }
       }
     }
 #pragma unroll
-    for (int i = 0; i < 12; ++i) Fcur[i] = Fnew[i];
-    if (MODE == OP_PCG) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) pown[c] = pown_next[c];
-    }
+    for (int c = 0; c < 3; ++c) own[c] = own_next[c];
+    mown = mown_next;
+  };
+
+  int it = 0;
+  for (; it + 1 < nit; it += 2) {
+    body(it, F0, F1, G0, G1);
+    body(it + 1, F1, F0, G1, G0);
   }
+  if (it < nit) body(it, F0, F1, G0, G1);
 
   if (MODE == OP_PCG) {
     const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
@@ -398,6 +464,7 @@ __global__ void __launch_bounds__(NT, 2) k_op(const OpArgs a) {
 }
 
 // ------------------------------------------------------------------ K_B and reductions
+// Flat over the padded vectors (pad entries of r and q are 0).
 // mode 0: init (r holds f - K u0): rr0, rz, convergence at k = 0
 // mode 1: iteration: r -= alpha q, beta = rz_new / rz, iters += 1, convergence
 // mode 2: true residual (r holds f - K u): rr_true
@@ -410,17 +477,35 @@ __global__ void __launch_bounds__(256) k_pcg_b(Grid g, double* __restrict__ r,
   if (mode == 1 && *(volatile int*)&s->done) return;
   const double alpha = (mode == 1) ? *(volatile double*)&s->alpha : 0.0;
   double rr = 0.0, rz = 0.0;
-  const long long n = g.ndof;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride) {
-    double rv = r[d];
+  const int n2 = (int)(g.ndof_pad / 2);  // ndof_pad is even
+  const int stride = gridDim.x * blockDim.x;
+  double2* r2 = reinterpret_cast<double2*>(r);
+  const double2* q2 = reinterpret_cast<const double2*>(q);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += 2 * stride) {
+    const int i1 = i + stride;
+    const bool has1 = i1 < n2;
+    double2 ra = r2[i], rb = has1 ? r2[i1] : make_double2(0.0, 0.0);
+    double da0 = __ldg(dinv + (2 * i) / 3), da1 = __ldg(dinv + (2 * i + 1) / 3);
+    double db0 = has1 ? __ldg(dinv + (2 * i1) / 3) : 0.0;
+    double db1 = has1 ? __ldg(dinv + (2 * i1 + 1) / 3) : 0.0;
     if (mode == 1) {
-      rv = fma(-alpha, q[d], rv);
-      r[d] = rv;
+      const double2 qa = q2[i];
+      const double2 qb = has1 ? q2[i1] : make_double2(0.0, 0.0);
+      ra.x = fma(-alpha, qa.x, ra.x);
+      ra.y = fma(-alpha, qa.y, ra.y);
+      rb.x = fma(-alpha, qb.x, rb.x);
+      rb.y = fma(-alpha, qb.y, rb.y);
+      r2[i] = ra;
+      if (has1) r2[i1] = rb;
     }
-    const double di = __ldg(dinv + d / 3);
-    rr = fma(rv, rv, rr);
-    rz = fma(di * rv, rv, rz);
+    rr = fma(ra.x, ra.x, rr);
+    rz = fma(da0 * ra.x, ra.x, rz);
+    rr = fma(ra.y, ra.y, rr);
+    rz = fma(da1 * ra.y, ra.y, rz);
+    rr = fma(rb.x, rb.x, rr);
+    rz = fma(db0 * rb.x, rb.x, rz);
+    rr = fma(rb.y, rb.y, rr);
+    rz = fma(db1 * rb.y, rb.y, rz);
   }
   const double brr = block_sum(rr, red);
   const double brz = block_sum(rz, red);
@@ -466,7 +551,7 @@ __global__ void k_scal_init(Scal* s, double tol_fnorm, int max_iters) {
   s->cntA = 0; s->cntB = 0; s->cntR = 0;
 }
 
-// r = -q, then r[load dof] += f (loads are distinct DOFs)
+// r = -q (padded), then r[load dof] += f (loads are distinct DOFs)
 __global__ void k_resid(long long n, const double* __restrict__ q, double* __restrict__ r) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride)
@@ -490,30 +575,51 @@ __global__ void k_finish(long long n, double* __restrict__ u, const double* __re
     u[d] = fma(alpha, p[d], u[d]);
 }
 
-__global__ void k_copy_masked(long long n, const double* __restrict__ src,
-                              double* __restrict__ dst, const uint8_t* __restrict__ mask) {
+// dense ABI vector -> padded internal vector, fixed entries zeroed
+__global__ void k_pack(Grid g, const double* __restrict__ dense, double* __restrict__ pad,
+                       const uint8_t* __restrict__ mask) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride) {
-    const bool fixed = (mask[d / 3] >> (d % 3)) & 1u;
-    dst[d] = fixed ? 0.0 : src[d];
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < g.nn; n += stride) {
+    const int i = (int)(n % g.nnx);
+    const int j = (int)((n / g.nnx) % g.nny);
+    const int k = (int)(n / ((long long)g.nnx * g.nny));
+    const unsigned m = mask ? mask[mask_index(g, i, j, k)] : 0u;  // NULL: no masking
+    const long long p = 3 * node_pad(g, i, j, k);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) pad[p + c] = ((m >> c) & 1u) ? 0.0 : dense[3 * n + c];
+  }
+}
+__global__ void k_unpack(Grid g, const double* __restrict__ pad, double* __restrict__ dense) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < g.nn; n += stride) {
+    const int i = (int)(n % g.nnx);
+    const int j = (int)((n / g.nnx) % g.nny);
+    const int k = (int)(n / ((long long)g.nnx * g.nny));
+    const long long p = 3 * node_pad(g, i, j, k);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) dense[3 * n + c] = pad[p + c];
   }
 }
 
 // ------------------------------------------------------------------ SIMP and Jacobi
-__global__ void k_simp(long long ne, const double* __restrict__ rho, double* __restrict__ E,
+// E (padded element rows) from the caller's dense rho; flags rho outside [0,1] or NaN.
+__global__ void k_simp(Grid g, const double* __restrict__ rho, double* __restrict__ E,
                        double E0, double Emin, double penal, Scal* s) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   bool bad = false;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ne; e += stride) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.ne; e += stride) {
+    const int i = (int)(e % g.nx);
+    const int j = (int)((e / g.nx) % g.ny);
+    const int k = (int)(e / ((long long)g.nx * g.ny));
     const double r = rho[e];
     bad |= !(r >= 0.0 && r <= 1.0);
-    E[e] = Emin + pow(r, penal) * (E0 - Emin);
+    E[elem_pad(g, i, j, k)] = Emin + pow(r, penal) * (E0 - Emin);
   }
   if (bad) s->domain_bad = 1;
 }
 
 // diag(K) at node n = KE_dd * sum of E over the (up to 8) elements around n; all 24
-// diagonal entries of the cube KE are equal, so D^-1 is one scalar per node.
+// diagonal entries of the cube KE are equal, so D^-1 is one scalar per node (padded).
 __global__ void k_jacobi(Grid g, const double* __restrict__ E, double ke_diag,
                          double* __restrict__ dinv) {
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -527,9 +633,9 @@ __global__ void k_jacobi(Grid g, const double* __restrict__ E, double ke_diag,
         for (int di = -1; di <= 0; ++di) {
           const int ei = i + di, ej = j + dj, ek = k + dk;
           if (ei >= 0 && ei < g.nx && ej >= 0 && ej < g.ny && ek >= 0 && ek < g.nz)
-            sE += E[ei + (long long)g.nx * (ej + (long long)g.ny * ek)];
+            sE += E[elem_pad(g, ei, ej, ek)];
         }
-    dinv[n] = 1.0 / (ke_diag * sE);
+    dinv[node_pad(g, i, j, k)] = 1.0 / (ke_diag * sE);
   }
 }
 
@@ -560,8 +666,10 @@ __global__ void __launch_bounds__(256) k_sens(Grid g, Walsh W, const double* __r
     double cv[8][3];
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
-      const long long n = corner_node(g, i, j, k, a);
-      const unsigned m = __ldg(mask + n);
+      int ax, ay, az;
+      corner_offset(a, ax, ay, az);
+      const long long n = node_dense(g, i + ax, j + ay, k + az);
+      const unsigned m = __ldg(mask + mask_index(g, i + ax, j + ay, k + az));
 #pragma unroll
       for (int c = 0; c < 3; ++c) cv[a][c] = ((m >> c) & 1u) ? 0.0 : __ldg(u + 3 * n + c);
     }
@@ -701,16 +809,33 @@ __global__ void k_edofs(Grid g, long long* map) {
     const int j = (int)((e / g.nx) % g.ny);
     const int k = (int)(e / ((long long)g.nx * g.ny));
     for (int a = 0; a < 8; ++a) {
-      const long long n = corner_node(g, i, j, k, a);
+      int ax, ay, az;
+      corner_offset(a, ax, ay, az);
+      const long long n = node_dense(g, i + ax, j + ay, k + az);
       for (int c = 0; c < 3; ++c) map[24 * e + 3 * a + c] = 3 * n + c;
     }
   }
 }
 
-__global__ void k_mask_dofs(long long ndof, const uint8_t* mask, uint8_t* out) {
+__global__ void k_mask_dofs(Grid g, const uint8_t* mask, uint8_t* out) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < ndof; d += stride)
-    out[d] = (mask[d / 3] >> (d % 3)) & 1u;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < g.nn; n += stride) {
+    const int i = (int)(n % g.nnx);
+    const int j = (int)((n / g.nnx) % g.nny);
+    const int k = (int)(n / ((long long)g.nnx * g.nny));
+    const unsigned m = mask[mask_index(g, i, j, k)];
+    for (int c = 0; c < 3; ++c) out[3 * n + c] = (m >> c) & 1u;
+  }
+}
+
+__global__ void k_dinv_dense(Grid g, const double* dinv_pad, double* out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < g.nn; n += stride) {
+    const int i = (int)(n % g.nnx);
+    const int j = (int)((n / g.nnx) % g.nny);
+    const int k = (int)(n / ((long long)g.nnx * g.nny));
+    out[n] = dinv_pad[node_pad(g, i, j, k)];
+  }
 }
 
 __global__ void k_dfma(double* out, int iters) {
@@ -739,51 +864,43 @@ inline unsigned nblk(long long n, int bs, int cap) {
 
 // ================================================================== launch helpers
 dim3 op_grid(const Grid& g, int nchunk) {
-  return dim3((unsigned)((g.nnx + OUTX - 1) / OUTX), (unsigned)((g.nny + OUTY - 1) / OUTY),
+  return dim3((unsigned)((g.nnx + OX - 1) / OX), (unsigned)((g.nny + OY - 1) / OY),
               (unsigned)nchunk);
 }
 
-static size_t op_smem(int mode) {
-  const int narr = mode == OP_PCG ? 4 : 1;
-  return sizeof(double) * ((size_t)SLOTS * narr * NT + NT + UPLANE + 9 * NT + 32) + 16;
+size_t op_smem(int /*mode*/) {
+  return sizeof(double) * ((size_t)NS * STAGE + IN_N + 9 * NT + 32) + sizeof(uint64_t) * NS + 16;
+}
+
+static void op_attr() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(k_op<OP_PCG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)op_smem(1));
+  cudaFuncSetAttribute(k_op<OP_APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)op_smem(0));
+  done = true;
 }
 
 cudaError_t launch_op(int mode, const OpArgs& a, dim3 grid, cudaStream_t st) {
-  static bool attr_done[2] = {false, false};
-  const size_t sm = op_smem(mode);
-  if (mode == OP_PCG) {
-    if (!attr_done[1]) {
-      cudaFuncSetAttribute(k_op<OP_PCG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr_done[1] = true;
-    }
-    k_op<OP_PCG><<<grid, dim3(TX, BY), sm, st>>>(a);
-  } else {
-    if (!attr_done[0]) {
-      cudaFuncSetAttribute(k_op<OP_APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sm);
-      attr_done[0] = true;
-    }
-    k_op<OP_APPLY><<<grid, dim3(TX, BY), sm, st>>>(a);
-  }
+  op_attr();
+  if (mode == OP_PCG) k_op<OP_PCG><<<grid, dim3(TX, BY), op_smem(1), st>>>(a);
+  else k_op<OP_APPLY><<<grid, dim3(TX, BY), op_smem(0), st>>>(a);
   return cudaGetLastError();
 }
 
 int op_occupancy(int mode) {
+  op_attr();
   int nb = 0;
-  const size_t sm = op_smem(mode);
-  if (mode == OP_PCG) {
-    cudaFuncSetAttribute(k_op<OP_PCG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_op<OP_PCG>, NT, sm);
-  } else {
-    cudaFuncSetAttribute(k_op<OP_APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_op<OP_APPLY>, NT, sm);
-  }
+  if (mode == OP_PCG)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_op<OP_PCG>, NT, op_smem(1));
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_op<OP_APPLY>, NT, op_smem(0));
   return nb;
 }
 
 cudaError_t launch_simp(const Grid& g, const double* rho, double* E, double E0, double Emin,
                         double penal, Scal* s, cudaStream_t st) {
-  k_simp<<<nblk(g.ne, 256, 148 * 16), 256, 0, st>>>(g.ne, rho, E, E0, Emin, penal, s);
+  k_simp<<<nblk(g.ne, 256, 148 * 16), 256, 0, st>>>(g, rho, E, E0, Emin, penal, s);
   return cudaGetLastError();
 }
 cudaError_t launch_jacobi(const Grid& g, const double* E, double ke_diag, double* dinv,
@@ -791,9 +908,13 @@ cudaError_t launch_jacobi(const Grid& g, const double* E, double ke_diag, double
   k_jacobi<<<nblk(g.nn, 256, 148 * 16), 256, 0, st>>>(g, E, ke_diag, dinv);
   return cudaGetLastError();
 }
-cudaError_t launch_copy_masked(const Grid& g, const double* src, double* dst,
-                               const uint8_t* mask, cudaStream_t st) {
-  k_copy_masked<<<nblk(g.ndof, 256, 148 * 16), 256, 0, st>>>(g.ndof, src, dst, mask);
+cudaError_t launch_pack(const Grid& g, const double* dense, double* pad, const uint8_t* mask,
+                        cudaStream_t st) {
+  k_pack<<<nblk(g.nn, 256, 148 * 16), 256, 0, st>>>(g, dense, pad, mask);
+  return cudaGetLastError();
+}
+cudaError_t launch_unpack(const Grid& g, const double* pad, double* dense, cudaStream_t st) {
+  k_unpack<<<nblk(g.nn, 256, 148 * 16), 256, 0, st>>>(g, pad, dense);
   return cudaGetLastError();
 }
 cudaError_t launch_scal_init(Scal* s, double tol_fnorm, int max_iters, cudaStream_t st) {
@@ -802,7 +923,7 @@ cudaError_t launch_scal_init(Scal* s, double tol_fnorm, int max_iters, cudaStrea
 }
 cudaError_t launch_resid(const Grid& g, const double* q, double* r, const int64_t* ldofs,
                          const double* lvals, int nloads, cudaStream_t st) {
-  k_resid<<<nblk(g.ndof, 256, 148 * 16), 256, 0, st>>>(g.ndof, q, r);
+  k_resid<<<nblk(g.ndof_pad, 256, 148 * 16), 256, 0, st>>>(g.ndof_pad, q, r);
   if (nloads > 0) k_add_loads<<<nblk(nloads, 256, 64), 256, 0, st>>>(r, ldofs, lvals, nloads);
   return cudaGetLastError();
 }
@@ -811,9 +932,9 @@ cudaError_t launch_pcg_b(const Grid& g, double* r, const double* q, const double
   k_pcg_b<<<nblocks, 256, 0, st>>>(g, r, q, dinv, s, partials, mode);
   return cudaGetLastError();
 }
-cudaError_t launch_finish(const Grid& g, double* u, const double* p0, const double* p1,
-                          const uint8_t* /*mask*/, Scal* s, cudaStream_t st) {
-  k_finish<<<nblk(g.ndof, 256, 148 * 16), 256, 0, st>>>(g.ndof, u, p0, p1, s);
+cudaError_t launch_finish(const Grid& g, double* u, const double* p0, const double* p1, Scal* s,
+                          cudaStream_t st) {
+  k_finish<<<nblk(g.ndof_pad, 256, 148 * 16), 256, 0, st>>>(g.ndof_pad, u, p0, p1, s);
   return cudaGetLastError();
 }
 cudaError_t launch_compliance(const double* u, const int64_t* ldofs, const double* lvals,
@@ -869,15 +990,17 @@ cudaError_t launch_edofs(const Grid& g, long long* map, cudaStream_t st) {
 }
 cudaError_t launch_mask_dofs(const Grid& g, const uint8_t* mask, uint8_t* out,
                              cudaStream_t st) {
-  k_mask_dofs<<<nblk(g.ndof, 256, 148 * 16), 256, 0, st>>>(g.ndof, mask, out);
+  k_mask_dofs<<<nblk(g.nn, 256, 148 * 16), 256, 0, st>>>(g, mask, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_dinv_dense(const Grid& g, const double* dinv_pad, double* out,
+                              cudaStream_t st) {
+  k_dinv_dense<<<nblk(g.nn, 256, 148 * 16), 256, 0, st>>>(g, dinv_pad, out);
   return cudaGetLastError();
 }
 cudaError_t launch_dfma(double* out, int blocks, int iters, cudaStream_t st) {
   k_dfma<<<blocks, 256, 0, st>>>(out, iters);
   return cudaGetLastError();
-}
-cudaError_t launch_zero(double* p, long long n, cudaStream_t st) {
-  return cudaMemsetAsync(p, 0, sizeof(double) * (size_t)n, st);
 }
 
 }  // namespace tomo

@@ -1,19 +1,38 @@
 // Internal declarations shared by the libtomo host code (api.cu) and the kernels
 // (kernels.cu). Not part of the ABI; see include/tomo.h.
 #pragma once
-#include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <cstdint>
 
 namespace tomo {
 
 // Structured grid of nx*ny*nz hexahedra; (nx+1)(ny+1)(nz+1) nodes.
+// The ABI vectors are dense (node n = i + nnx(j + nny k)). The solver's internal vectors
+// use a PADDED layout: node rows of nnx_pad (even) nodes so that a row of 3-DOF nodes is a
+// multiple of 16 bytes (a TMA requirement); element fields use rows of nx_pad (even);
+// the per-node fixed mask uses byte rows of mp (multiple of 16).
 struct Grid {
   int nx, ny, nz;     // elements per axis
   int nnx, nny, nnz;  // nodes per axis
-  long long nn;       // nodes
-  long long ne;       // elements
-  long long ndof;     // 3 * nn
+  int nnx_pad, nx_pad, mp;
+  long long nn, ne, ndof;          // dense counts
+  long long nn_pad, ne_pad, ndof_pad, mask_bytes;
 };
+
+__host__ __device__ inline long long node_pad(const Grid& g, int i, int j, int k) {
+  return (long long)i + (long long)g.nnx_pad * (j + (long long)g.nny * k);
+}
+__host__ __device__ inline long long node_dense(const Grid& g, int i, int j, int k) {
+  return (long long)i + (long long)g.nnx * (j + (long long)g.nny * k);
+}
+__host__ __device__ inline long long mask_index(const Grid& g, int i, int j, int k) {
+  return (long long)i + (long long)g.mp * (j + (long long)g.nny * k);
+}
+__host__ __device__ inline long long elem_pad(const Grid& g, int i, int j, int k) {
+  return (long long)i + (long long)g.nx_pad * (j + (long long)g.ny * k);
+}
 
 // The E=1 element stiffness KE written in the (unnormalised, +-1) tensor-Walsh basis of
 // corner values: D = T KE T^T / 64 has 45 non-zeros out of 576, described by these seven
@@ -50,40 +69,52 @@ struct Scal {
 
 enum OpMode { OP_APPLY = 0, OP_PCG = 1 };
 
+// Operator tile: 32 x OP_BY threads; thread (tx, ty) owns element column
+// (i0-1+tx, j0-1+ty) for tx < 31, and output node (i0+tx, j0+ty) for tx < OP_OX,
+// ty < OP_OY. A block marches along z through a chunk of node planes.
+constexpr int OP_BY = 8;
+constexpr int OP_OX = 30;           // output nodes per tile along x (even: 16-B TMA rows)
+constexpr int OP_OY = OP_BY - 1;    // output nodes per tile along y
+constexpr int OP_NS = 3;            // TMA pipeline stages (node planes in flight)
+
 struct OpArgs {
+  CUtensorMap tm_in;    // APPLY: u ; PCG: r   (box 96 x (BY+1) doubles)
+  CUtensorMap tm_pold;  // PCG: p_{k-1}        (box 96 x (BY+1))
+  CUtensorMap tm_uown;  // PCG: u, owned box   (box 90 x BY-1)
+  CUtensorMap tm_dinv;  // PCG: Jacobi, per node (box 32 x (BY+1))
+  CUtensorMap tm_mask;  // fixed mask bytes     (box 32 x (BY+1))
+  CUtensorMap tm_E;     // element modulus      (box 32 x BY)
   Grid g;
   Walsh w;
-  const double* E;       // N_e
-  const uint8_t* mask;   // N_n, bit c = DOF 3n+c fixed
-  const double* in;      // APPLY: u ; PCG: r
-  const double* pold;    // PCG: p_{k-1}
-  double* pnew;          // PCG: p_k (owned nodes written)
-  double* u;             // PCG: u (owned nodes: u += alpha_{k-1} p_{k-1})
-  const double* dinv;    // PCG: Jacobi, N_n
-  double* out;           // APPLY: y ; PCG: q
-  double* partials;      // PCG: one per block
-  Scal* s;               // PCG
-  int nchunk;            // z chunks (gridDim.z)
+  double* pnew;         // PCG: p_k (owned nodes written)
+  double* u;            // PCG: u (owned nodes: u += alpha_{k-1} p_{k-1})
+  double* out;          // APPLY: y (raw u at fixed DOFs) ; PCG: q
+  double* partials;     // PCG: one per block
+  Scal* s;              // PCG
+  int nchunk;           // z chunks (gridDim.z)
 };
 
-// launch helpers (kernels.cu). All enqueue on `st`; return cudaGetLastError().
-constexpr int OP_BY = 8;  // threads per block = 32 * OP_BY
+// launch helpers (kernels.cu). All enqueue on `st`; return the launch error.
 dim3 op_grid(const Grid& g, int nchunk);
+size_t op_smem(int mode);
+int op_occupancy(int mode);
 cudaError_t launch_op(int mode, const OpArgs& a, dim3 grid, cudaStream_t st);
 cudaError_t launch_simp(const Grid& g, const double* rho, double* E, double E0, double Emin,
                         double penal, Scal* s, cudaStream_t st);
 cudaError_t launch_jacobi(const Grid& g, const double* E, double ke_diag, double* dinv,
                           cudaStream_t st);
-cudaError_t launch_copy_masked(const Grid& g, const double* src, double* dst,
-                               const uint8_t* mask, cudaStream_t st);
+// dense ABI vector <-> padded internal vector (in: fixed entries zeroed)
+cudaError_t launch_pack(const Grid& g, const double* dense, double* pad, const uint8_t* mask,
+                        cudaStream_t st);
+cudaError_t launch_unpack(const Grid& g, const double* pad, double* dense, cudaStream_t st);
 cudaError_t launch_scal_init(Scal* s, double tol_fnorm, int max_iters, cudaStream_t st);
-// r = -q + f (sparse f), then rr / rz reductions (mode 0: init, 2: true residual)
-cudaError_t launch_resid(const Grid& g, const double* q, double* r, const int64_t* ldofs,
+// r = -q + f (sparse f at padded DOF indices)
+cudaError_t launch_resid(const Grid& g, const double* q, double* r, const int64_t* ldofs_pad,
                          const double* lvals, int nloads, cudaStream_t st);
 cudaError_t launch_pcg_b(const Grid& g, double* r, const double* q, const double* dinv,
                          Scal* s, double* partials, int nblocks, int mode, cudaStream_t st);
-cudaError_t launch_finish(const Grid& g, double* u, const double* p0, const double* p1,
-                          const uint8_t* mask, Scal* s, cudaStream_t st);
+cudaError_t launch_finish(const Grid& g, double* u, const double* p0, const double* p1, Scal* s,
+                          cudaStream_t st);
 cudaError_t launch_compliance(const double* u, const int64_t* ldofs, const double* lvals,
                               int nloads, Scal* s, cudaStream_t st);
 cudaError_t launch_sens(const Grid& g, const Walsh& w, const double* rho, const double* u,
@@ -102,7 +133,8 @@ int oc_max_blocks();
 cudaError_t launch_edofs(const Grid& g, long long* map, cudaStream_t st);
 cudaError_t launch_mask_dofs(const Grid& g, const uint8_t* mask, uint8_t* out,
                              cudaStream_t st);
+cudaError_t launch_dinv_dense(const Grid& g, const double* dinv_pad, double* out,
+                              cudaStream_t st);
 cudaError_t launch_dfma(double* out, int blocks, int iters, cudaStream_t st);
-cudaError_t launch_zero(double* p, long long n, cudaStream_t st);
 
 }  // namespace tomo
