@@ -39,17 +39,16 @@ struct tomo_ctx {
   cudaStream_t st = nullptr;
   char* ws = nullptr;
   size_t ws_bytes = 0;
-  size_t off_E, off_dinv, off_Hs, off_t0, off_t1, off_t2, off_u, off_r, off_p0, off_p1, off_q, off_us,
+  size_t off_E, off_dinv, off_Hs, off_t0, off_t1, off_t2, off_u, off_r0, off_r1, off_p0, off_p1, off_q0, off_q1, off_us,
       off_mask, off_cnt, off_ld, off_ldp, off_lv, off_taps, off_tw, off_part, off_scal, off_oc,
       off_end;
   size_t n_part = 0;
-  int nchunk = 1;
-  dim3 opg;
+  int op_blocks = 1;
   int nb_b = 1, nb_s = 1, nb_oc = 1;
   int64_t launches = 0;
   int sms = 148;
   // operator launch variants (tensor maps bound to workspace buffers)
-  OpArgs op_apply_u{}, op_apply_p0{}, op_pcg_odd{}, op_pcg_even{};
+  OpArgs op_apply_u{}, op_apply_p0{}, op_pcg[2];  // op_pcg[k & 1] for launch k
   // profiling
   bool prof = false;
   double prof_a_ms = 0, prof_b_ms = 0;
@@ -65,9 +64,9 @@ struct tomo_ctx {
   double* t1() const { return P<double>(off_t1); }
   double* t2() const { return P<double>(off_t2); }
   double* u() const { return P<double>(off_u); }
-  double* r() const { return P<double>(off_r); }
+  double* r(int i) const { return P<double>(i ? off_r1 : off_r0); }
   double* p(int i) const { return P<double>(i ? off_p1 : off_p0); }
-  double* q() const { return P<double>(off_q); }
+  double* q(int i) const { return P<double>(i ? off_q1 : off_q0); }
   double* us() const { return P<double>(off_us); }
   uint8_t* dmask() const { return P<uint8_t>(off_mask); }
   int* cnt() const { return P<int>(off_cnt); }
@@ -377,10 +376,12 @@ extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, doubl
   c->off_t1 = take(ve);
   c->off_t2 = take(ve);
   c->off_u = take(vp);
-  c->off_r = take(vp);
+  c->off_r0 = take(vp);
+  c->off_r1 = take(vp);
   c->off_p0 = take(vp);
   c->off_p1 = take(vp);
-  c->off_q = take(vp);
+  c->off_q0 = take(vp);
+  c->off_q1 = take(vp);
   c->off_us = take(sizeof(double) * (size_t)g.ndof);
   c->off_mask = take((size_t)g.mask_bytes);
   c->off_cnt = take(sizeof(int) * (size_t)g.ne);
@@ -389,9 +390,7 @@ extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, doubl
   c->off_lv = take(sizeof(double) * (c->load_dofs.size() + 1));
   c->off_taps = take(sizeof(int) * (c->taps.size() + 3));
   c->off_tw = take(sizeof(double) * (c->tap_w.size() + 1));
-  const dim3 og = op_grid(g, 1);
-  size_t maxb = (size_t)og.x * og.y * (size_t)std::min(g.nnz, 64);
-  c->n_part = std::max<size_t>(maxb, 8192) * 2;
+  c->n_part = 8192 * 5;
   c->off_part = take(sizeof(double) * c->n_part);
   c->off_scal = take(sizeof(Scal));
   c->off_oc = take(sizeof(double) * 4);
@@ -428,20 +427,22 @@ int build_op_args(tomo_ctx* c) {
   const uint64_t rowm = (uint64_t)g.mp, planem = rowm * g.nny;
   const uint64_t rowe = 8ull * g.nx_pad, planee = rowe * g.ny;
   const CUtensorMapDataType F64 = CU_TENSOR_MAP_DATA_TYPE_FLOAT64, U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
-  const uint32_t inw = 3 * (OP_OX + 2) + 2, inh = OP_BY + 1;  // boxes widened: aligned starts
-  CUtensorMap tm_u, tm_uown, tm_r, tm_p0, tm_p1, tm_dinv, tm_mask, tm_E;
+  const uint32_t inw = 3 * (OP_OX + 2) + 2, inh = OP_BY;  // boxes widened: aligned starts
+  CUtensorMap tm_u, tm_uown, tm_r[2], tm_q[2], tm_p[2], tm_dinv, tm_mask, tm_E;
   int rc;
   auto vec = [&](CUtensorMap* tm, double* base, uint32_t b0, uint32_t b1) {
     return make_map(c, tm, F64, base, 3ull * g.nnx, g.nny, g.nnz, rowv, planev, b0, b1);
   };
   if ((rc = vec(&tm_u, c->u(), inw, inh))) return rc;
   if ((rc = vec(&tm_uown, c->u(), 3 * OP_OX, OP_OY))) return rc;
-  if ((rc = vec(&tm_r, c->r(), inw, inh))) return rc;
-  if ((rc = vec(&tm_p0, c->p(0), inw, inh))) return rc;
-  if ((rc = vec(&tm_p1, c->p(1), inw, inh))) return rc;
+  for (int i = 0; i < 2; ++i) {
+    if ((rc = vec(&tm_r[i], c->r(i), inw, inh))) return rc;
+    if ((rc = vec(&tm_q[i], c->q(i), inw, inh))) return rc;
+    if ((rc = vec(&tm_p[i], c->p(i), inw, inh))) return rc;
+  }
   if ((rc = make_map(c, &tm_dinv, F64, c->dinv(), g.nnx, g.nny, g.nnz, rown, planen, OP_OX + 4, inh))) return rc;
   if ((rc = make_map(c, &tm_mask, U8, c->dmask(), g.nnx, g.nny, g.nnz, rowm, planem, 48, inh))) return rc;
-  if ((rc = make_map(c, &tm_E, F64, c->E(), g.nx, g.ny, g.nz, rowe, planee, 32, OP_BY))) return rc;
+  if ((rc = make_map(c, &tm_E, F64, c->E(), g.nx, g.ny, g.nz, rowe, planee, 32, OP_BY - 1))) return rc;
   OpArgs base{};
   base.tm_uown = tm_uown;
   base.tm_dinv = tm_dinv;
@@ -451,23 +452,26 @@ int build_op_args(tomo_ctx* c) {
   base.w = c->w;
   base.partials = c->part();
   base.s = c->scal();
-  base.nchunk = c->nchunk;
+  base.ntiles = op_tiles(g);
   c->op_apply_u = base;
   c->op_apply_u.tm_in = tm_u;
-  c->op_apply_u.out = c->q();
+  c->op_apply_u.out = c->q(0);
   c->op_apply_p0 = base;
-  c->op_apply_p0.tm_in = tm_p0;
-  c->op_apply_p0.out = c->q();
-  // iteration k (1-based): p_old = p[(k-1)&1], p_new = p[k&1]
-  c->op_pcg_odd = base;
-  c->op_pcg_odd.tm_in = tm_r;
-  c->op_pcg_odd.tm_pold = tm_p0;
-  c->op_pcg_odd.pnew = c->p(1);
-  c->op_pcg_odd.u = c->u();
-  c->op_pcg_odd.out = c->q();
-  c->op_pcg_even = c->op_pcg_odd;
-  c->op_pcg_even.tm_pold = tm_p1;
-  c->op_pcg_even.pnew = c->p(0);
+  c->op_apply_p0.tm_in = tm_p[0];
+  c->op_apply_p0.out = c->q(0);
+  // launch k reads the "old" buffers (k & 1) ^ 1 and writes the "new" ones k & 1
+  for (int par = 0; par < 2; ++par) {
+    const int o = par ^ 1, n = par;
+    OpArgs& a = c->op_pcg[par];
+    a = base;
+    a.tm_in = tm_r[o];
+    a.tm_qold = tm_q[o];
+    a.tm_pold = tm_p[o];
+    a.rnew = c->r(n);
+    a.pnew = c->p(n);
+    a.out = c->q(n);
+    a.u = c->u();
+  }
   return TOMO_OK;
 }
 }  // namespace
@@ -500,25 +504,13 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
     CK(c, cudaMemcpyAsync(c->tw(), c->tap_w.data(), sizeof(double) * c->tap_w.size(), cudaMemcpyHostToDevice, c->st));
   }
   LAUNCH(c, launch_filter_sums(g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), c->cnt(), c->st));
-  // z-chunking of the operator grid: minimise waves x planes per block
-  const dim3 og = op_grid(g, 1);
-  const long long tiles = (long long)og.x * og.y;
+  // persistent operator grid: one block per resident slot, each with an equal share of
+  // the (tile, node plane) work list; at least ~6 planes per block on small grids
   int occ = op_occupancy(OP_PCG);
   if (occ < 1) occ = 1;
-  const long long slots = (long long)occ * c->sms;
-  double best = 1e300;
-  int bestc = 1;
-  const int cmax = std::min(g.nnz, 64);
-  for (int ch = 1; ch <= cmax; ++ch) {
-    if ((size_t)tiles * ch > c->n_part / 2) break;
-    const long long waves = (tiles * ch + slots - 1) / slots;
-    const double planes = std::ceil((double)g.nnz / ch) + 2.0;
-    const double cost = waves * planes;
-    if (cost < best - 1e-9) { best = cost; bestc = ch; }
-  }
-  c->nchunk = bestc;
-  c->opg = op_grid(g, bestc);
-  c->nb_b = (int)std::min<long long>((g.ndof_pad / 2 + 511) / 512, (long long)c->sms * 8);
+  const long long units = (long long)op_tiles(g) * g.nnz;
+  c->op_blocks = (int)std::max<long long>(1, std::min<long long>((long long)occ * c->sms, units / 6));
+  c->nb_b = (int)std::min<long long>((g.ndof_pad / 2 + 255) / 256, (long long)c->sms * 4);
   c->nb_s = (int)std::min<long long>((g.ne + 255) / 256, (long long)c->sms * 8);
   c->nb_oc = std::min(oc_max_blocks(), (int)std::max<long long>(1, (g.ne + 255) / 256));
   if ((size_t)c->nb_oc * 2 > c->n_part) c->nb_oc = (int)(c->n_part / 2);
@@ -550,69 +542,62 @@ int prepare_modulus(tomo_ctx* c, const double* d_rho, bool jacobi) {
   return TOMO_OK;
 }
 
-// PCG on the bound workspace: E / dinv ready; c->u() holds x0 (padded, masked).
+// Single-pass Jacobi-PCG on the bound workspace: E / dinv ready; c->u()
+// holds x0 (padded, masked). One fused launch per iteration; launch k checks r_k.
 int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) {
   const Grid& g = c->g;
   const int nl = (int)c->load_dofs.size();
+  const size_t vb = sizeof(double) * (size_t)g.ndof_pad;
   Scal hs{};
   LAUNCH(c, launch_scal_init(c->scal(), tol * c->fnorm, max_iters, c->st));
-  // r0 = f - K u0 ; rr0, rz0
-  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->opg, c->st));
-  LAUNCH(c, launch_resid(g, c->q(), c->r(), c->ldp(), c->lv(), nl, c->st));
-  LAUNCH(c, launch_pcg_b(g, c->r(), c->q(), c->dinv(), c->scal(), c->part(), c->nb_b, 0, c->st));
-  CK(c, cudaMemsetAsync(c->p(0), 0, sizeof(double) * (size_t)g.ndof_pad, c->st));
-  int k = 0;  // iterations launched
+  // r_{-1} := r0 = f - K u0 in r[1]; q_{-1} = p_{-1} = 0
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));
+  LAUNCH(c, launch_resid(g, c->q(0), c->r(1), c->ldp(), c->lv(), nl, c->st));
+  CK(c, cudaMemsetAsync(c->q(1), 0, vb, c->st));
+  CK(c, cudaMemsetAsync(c->p(1), 0, vb, c->st));
+  int k = 0;  // launches issued
   int batch = 8;
   const bool prof = c->prof;
   if (prof) {
-    const size_t need = 4 * 256;
-    while (c->ev.size() < need) {
+    while (c->ev.size() < 2 * 257) {
       cudaEvent_t e;
       CK(c, cudaEventCreate(&e));
       c->ev.push_back(e);
     }
   }
   for (;;) {
+    const int nb = std::min(batch, max_iters + 1 - k);
+    if (nb <= 0) break;
+    for (int i = 0; i < nb; ++i) {
+      if (prof && i < 256) CK(c, cudaEventRecord(c->ev[2 * i], c->st));
+      LAUNCH(c, launch_op(OP_PCG, c->op_pcg[(k + i) & 1], c->op_blocks, c->st));
+      if (prof && i < 256) CK(c, cudaEventRecord(c->ev[2 * i + 1], c->st));
+    }
+    const int k_before = hs.k;
+    k += nb;
     CK(c, cudaMemcpyAsync(&hs, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
     CK(c, cudaStreamSynchronize(c->st));
-    if (hs.done || k >= max_iters) break;
-    const int nb = std::min(batch, max_iters - k);
-    for (int i = 0; i < nb; ++i) {
-      const int it = k + i + 1;  // 1-based iteration
-      const OpArgs& a = (it & 1) ? c->op_pcg_odd : c->op_pcg_even;
-      if (prof && i < 256) CK(c, cudaEventRecord(c->ev[4 * i], c->st));
-      LAUNCH(c, launch_op(OP_PCG, a, c->opg, c->st));
-      if (prof && i < 256) CK(c, cudaEventRecord(c->ev[4 * i + 1], c->st));
-      LAUNCH(c, launch_pcg_b(g, c->r(), c->q(), c->dinv(), c->scal(), c->part(), c->nb_b, 1, c->st));
-      if (prof && i < 256) CK(c, cudaEventRecord(c->ev[4 * i + 2], c->st));
-    }
-    const int iters_before = hs.iters;
-    k += nb;
     if (prof) {
-      Scal h2{};
-      CK(c, cudaMemcpyAsync(&h2, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
-      CK(c, cudaStreamSynchronize(c->st));
-      const int real = std::min(h2.iters - iters_before, std::min(nb, 256));
-      for (int i = 0; i < real; ++i) {
-        float ta = 0, tb = 0;
-        CK(c, cudaEventElapsedTime(&ta, c->ev[4 * i], c->ev[4 * i + 1]));
-        CK(c, cudaEventElapsedTime(&tb, c->ev[4 * i + 1], c->ev[4 * i + 2]));
+      // launches that did work: up to and including the one that set `done`
+      const int real = std::min(nb, hs.done ? hs.iters - k_before + 1 : nb);
+      for (int i = 0; i < real && i < 256; ++i) {
+        float ta = 0;
+        CK(c, cudaEventElapsedTime(&ta, c->ev[2 * i], c->ev[2 * i + 1]));
         c->prof_a_ms += ta;
-        c->prof_b_ms += tb;
         ++c->prof_n;
       }
     }
+    if (hs.done) break;
     if (batch < 128) batch *= 2;
   }
   if (hs.done == 3) {
     return fail(c, hs.status ? hs.status : TOMO_EBREAKDOWN,
                 hs.status == TOMO_ENAN ? "NaN/Inf in PCG" : "PCG breakdown: p^T K p <= 0 (SPEC.md l.173)");
   }
-  LAUNCH(c, launch_finish(g, c->u(), c->p(0), c->p(1), c->scal(), c->st));
   // true residual ||f - K u||
-  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->opg, c->st));
-  LAUNCH(c, launch_resid(g, c->q(), c->p(0), c->ldp(), c->lv(), nl, c->st));
-  LAUNCH(c, launch_pcg_b(g, c->p(0), c->q(), c->dinv(), c->scal(), c->part(), c->nb_b, 2, c->st));
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));
+  LAUNCH(c, launch_resid(g, c->q(0), c->r(0), c->ldp(), c->lv(), nl, c->st));
+  LAUNCH(c, launch_norm2(g, c->r(0), c->scal(), c->part(), c->nb_b, c->st));
   CK(c, cudaMemcpyAsync(&hs, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
   CK(c, cudaStreamSynchronize(c->st));
   if (info) {
@@ -635,8 +620,8 @@ extern "C" int tomo_apply(tomo_ctx* c, const double* d_rho, int64_t n_e, const d
   if (d_u == d_y) return fail(c, TOMO_EINVAL, "u and y must not alias");
   if (int rc = prepare_modulus(c, d_rho, false)) return rc;
   LAUNCH(c, launch_pack(c->g, d_u, c->p(0), nullptr, c->st));
-  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_p0, c->opg, c->st));
-  LAUNCH(c, launch_unpack(c->g, c->q(), d_y, c->st));
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_p0, c->op_blocks, c->st));
+  LAUNCH(c, launch_unpack(c->g, c->q(0), d_y, c->st));
   return TOMO_OK;
 }
 
@@ -872,7 +857,7 @@ extern "C" int tomo_set_profiling(tomo_ctx* c, int on) {
 extern "C" int tomo_profile_times(const tomo_ctx* c, double* t) {
   if (!c || !t) return TOMO_EINVAL;
   t[0] = c->prof_n ? c->prof_a_ms / c->prof_n : 0.0;
-  t[1] = c->prof_n ? c->prof_b_ms / c->prof_n : 0.0;
+  t[1] = 0.0;  // single-pass PCG: there is no separate K_B kernel
   t[2] = (double)c->prof_n;
   return TOMO_OK;
 }

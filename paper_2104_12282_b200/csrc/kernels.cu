@@ -35,35 +35,37 @@ constexpr int NT = TX * BY;            // threads per operator block
 constexpr int OX = OP_OX;              // output nodes per tile along x
 constexpr int OY = OP_OY;              // output nodes per tile along y
 constexpr int NS = OP_NS;              // pipeline stages
-constexpr int IN_W = 3 * (OX + 2);     // 96 doubles per input row (32 nodes) in U
-constexpr int IN_H = BY + 1;           // 9 input rows
-constexpr int IN_N = IN_W * IN_H;      // 864
+constexpr int NR = BY;                 // node rows per tile (one per warp)
+constexpr int ER = BY - 1;             // element rows per tile
 constexpr int OWN_W = 3 * OX;          // 90 doubles per owned row
-constexpr int OWN_N = OWN_W * OY;      // 630
+constexpr int OWN_N = OWN_W * OY;      // 540
 // TMA boxes. The innermost box start must be 16-byte aligned (measured on this B200: an
 // 8-byte-aligned start faults with "illegal instruction"), so every box starts at the
 // aligned-down coordinate and is widened; smem reads add the per-block offset.
-constexpr int VB_W = IN_W + 2;         // 98 doubles: vector rows (start offset 0..1)
+constexpr int VB_W = 3 * (OX + 2) + 2; // 98 doubles: vector rows (start offset 0..1)
 constexpr int DB_W = OX + 4;           // 34 doubles: Jacobi rows (start offset 0..1)
 constexpr int MB_W = 48;               // 48 bytes: mask rows (start offset 0..15)
-constexpr int E_W = 32, E_H = BY;      // element box (start offset 0..1, 31 columns used)
+constexpr int E_W = 32;                // element box width (start offset 0..1, 31 used)
 // stage layout in doubles, every piece 128-byte aligned
-constexpr int R_OFF = 0;
-constexpr int PO_OFF = 896;            // 882 used
-constexpr int UO_OFF = 1792;           // 630 used
-constexpr int DI_OFF = 2432;           // 306 used
-constexpr int EE_OFF = 2752;           // 256 used
-constexpr int MK_OFF = 3008;           // 432 bytes used
-constexpr int STAGE = 3072;            // 24576 B
-static_assert(PO_OFF >= VB_W * IN_H && UO_OFF - PO_OFF >= VB_W * IN_H && DI_OFF - UO_OFF >= OWN_N &&
-                  EE_OFF - DI_OFF >= DB_W * IN_H && MK_OFF - EE_OFF >= E_W * E_H &&
-                  (STAGE - MK_OFF) * 8 >= MB_W * IN_H,
+constexpr int R_OFF = 0;               // r_{k-1} (APPLY: u), 784 used
+constexpr int QO_OFF = 784;            // q_{k-1}, 784 used
+constexpr int PO_OFF = 1568;           // p_{k-1}, 784 used
+constexpr int UO_OFF = 2352;           // u, owned box, 540 used
+constexpr int DI_OFF = 2896;           // D^-1, 272 used
+constexpr int EE_OFF = 3168;           // E, 224 used
+constexpr int MK_OFF = 3392;           // mask, 384 bytes used
+constexpr int STAGE = 3456;            // 27648 B
+static_assert(QO_OFF >= VB_W * NR && PO_OFF - QO_OFF >= VB_W * NR &&
+                  UO_OFF - PO_OFF >= VB_W * NR && DI_OFF - UO_OFF >= OWN_N &&
+                  EE_OFF - DI_OFF >= DB_W * NR && MK_OFF - EE_OFF >= E_W * ER &&
+                  (STAGE - MK_OFF) * 8 >= MB_W * NR,
               "stage pieces overlap");
-static_assert((PO_OFF * 8) % 128 == 0 && (UO_OFF * 8) % 128 == 0 && (DI_OFF * 8) % 128 == 0 &&
-                  (EE_OFF * 8) % 128 == 0 && (MK_OFF * 8) % 128 == 0 && (STAGE * 8) % 128 == 0,
+static_assert((QO_OFF * 8) % 128 == 0 && (PO_OFF * 8) % 128 == 0 && (UO_OFF * 8) % 128 == 0 &&
+                  (DI_OFF * 8) % 128 == 0 && (EE_OFF * 8) % 128 == 0 && (MK_OFF * 8) % 128 == 0 &&
+                  (STAGE * 8) % 128 == 0,
               "TMA destinations must stay 128-byte aligned");
-constexpr unsigned BYTES_PCG = 8u * (2 * VB_W * IN_H + OWN_N + DB_W * IN_H + E_W * E_H) + MB_W * IN_H;
-constexpr unsigned BYTES_APPLY = 8u * (VB_W * IN_H + E_W * E_H) + MB_W * IN_H;
+constexpr unsigned BYTES_PCG = 8u * (3 * VB_W * NR + OWN_N + DB_W * NR + E_W * ER) + MB_W * NR;
+constexpr unsigned BYTES_APPLY = 8u * (VB_W * NR + E_W * ER) + MB_W * NR;
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -143,6 +145,32 @@ __device__ __forceinline__ double sum_partials(const double* p, int n, int strid
   double acc = 0.0;
   for (int i = t; i < n; i += nt) acc += __ldcg(p + (long long)i * stride + off);
   return block_sum(acc, red);
+}
+
+// Five deterministic block sums at once (one pass of barriers); result in every thread.
+__device__ __forceinline__ void block_sum5(double (&v)[5], double* red) {
+  const int t = threadIdx.x + blockDim.x * threadIdx.y;
+  const int nw = (blockDim.x * blockDim.y) >> 5;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if ((t & 31) == 0) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) red[i * 32 + (t >> 5)] = v[i];
+  }
+  __syncthreads();
+  if (t < 32) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      double r = (t < nw) ? red[i * 32 + t] : 0.0;
+      r = warp_sum(r);
+      if (t == 0) red[160 + i] = r;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 5; ++i) v[i] = red[160 + i];
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ Walsh element core
@@ -269,6 +297,7 @@ __device__ __forceinline__ void issue_plane(const OpArgs& a, double* stg, uint64
   mbar_expect_tx(bar, MODE == OP_PCG ? BYTES_PCG : BYTES_APPLY);
   tma_load_3d(stg + R_OFF, &a.tm_in, o.xv, j0 - 1, kq, bar);
   if (MODE == OP_PCG) {
+    tma_load_3d(stg + QO_OFF, &a.tm_qold, o.xv, j0 - 1, kq, bar);
     tma_load_3d(stg + PO_OFF, &a.tm_pold, o.xv, j0 - 1, kq, bar);
     tma_load_3d(stg + UO_OFF, &a.tm_uown, 3 * i0, j0, kq, bar);
     tma_load_3d(stg + DI_OFF, &a.tm_dinv, o.xd, j0 - 1, kq, bar);
@@ -281,10 +310,12 @@ template <int MODE>
 __global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) {
   extern __shared__ __align__(128) double smem[];
   double* stages = smem;                     // [NS][STAGE]
-  double* U = stages + NS * STAGE;           // [IN_N] current node plane (masked p / u)
-  double* S = U + IN_N;                      // [9][NT] corner contributions y00,y01,y10
-  double* red = S + 9 * NT;                  // [32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 32);  // [NS]
+  double* XE = stages + NS * STAGE;          // [2][6][NT] x-edge sums / differences (by plane parity)
+  double* CD = XE + 12 * NT;                 // [3][NT] row-ty contributions to row ty-1
+  double* GS = CD + 3 * NT;                  // [12][NT] thread-private: top-face sums of the last element
+  double* ACC = GS + 12 * NT;                // [5][NT] thread-private reduction accumulators
+  double* red = ACC + 5 * NT;                // [168]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 168);  // [NS]
   int* s_flag = reinterpret_cast<int*>(bars + NS);
 
   const int tx = threadIdx.x, ty = threadIdx.y, t = ty * TX + tx;
@@ -297,164 +328,220 @@ __global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) 
     alpha_prev = *(volatile double*)&a.s->alpha;
   }
 
-  const int i0 = blockIdx.x * OX, j0 = blockIdx.y * OY;
-  const int kbeg = (int)(((long long)blockIdx.z * g.nnz) / a.nchunk);
-  const int kend = (int)(((long long)(blockIdx.z + 1) * g.nnz) / a.nchunk);
-  const int nit = kend - kbeg + 2;
-  const bool colv = tx < OX + 1;  // element column inside the tile (lane 31 idles)
-  const bool outv = tx < OX && ty < OY && (i0 + tx) <= g.nx && (j0 + ty) <= g.ny;
-  const long long rowd = 3LL * g.nnx_pad;
-  const long long planed = rowd * g.nny;
-  const TileOrigin org = tile_origin(i0);
+  // 32-bit offsets into the padded vectors (ndof_pad < 2^31 is checked at create)
+  const int rowd = 3 * g.nnx_pad;
+  const int planed = rowd * g.nny;
+  // persistent, balanced schedule: block b owns work units [ub, ue) of the list
+  // (tile, node plane), tile-major; it processes them as z-segments split at tile edges
+  const int tiles_x = (g.nnx + OX - 1) / OX;
+  const long long units = (long long)a.ntiles * g.nnz;
+  const int ub = (int)((units * blockIdx.x) / gridDim.x);
+  const int ue = (int)((units * (blockIdx.x + 1)) / gridDim.x);
 
   if (t == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+#pragma unroll
+  for (int q = 0; q < 5; ++q) ACC[q * NT + t] = 0.0;
   __syncthreads();
+
+  int git = 0;  // global step counter (mbarrier phase)
+  for (int u0 = ub; u0 < ue;) {
+  const int tile = u0 / g.nnz;
+  const int kbeg = u0 - tile * g.nnz;
+  const int kend = min(g.nnz, kbeg + (ue - u0));
+  u0 += kend - kbeg;
+  const int i0 = (tile % tiles_x) * OX, j0 = (tile / tiles_x) * OY;
+  const int nit = kend - kbeg + 2;
+  const TileOrigin org = tile_origin(i0);
   if (t == 0) {
     for (int s = 0; s < NS && s < nit; ++s)
-      issue_plane<MODE>(a, stages + s * STAGE, &bars[s], org, i0, j0, kbeg - 1 + s);
+      issue_plane<MODE>(a, stages + ((git + s) % NS) * STAGE, &bars[(git + s) % NS], org, i0, j0,
+                        kbeg - 1 + s);
   }
 
-  double F0[12], F1[12], G0[12], G1[12];
-#pragma unroll
-  for (int i = 0; i < 12; ++i) { F0[i] = 0.0; F1[i] = 0.0; G0[i] = 0.0; G1[i] = 0.0; }
-  double own[3] = {0.0, 0.0, 0.0};  // PCG: p of the own node ; APPLY: raw u of the own node
-  unsigned mown = 0;                // fixed bits of the own node
-  double pq = 0.0;
-  const int f_own = (ty + 1) * IN_W + 3 * (tx + 1);                 // in U
-  const int v_own = (ty + 1) * VB_W + org.ov + 3 * (tx + 1);         // in the vector box
-  const int m_own = (ty + 1) * MB_W + org.om + tx + 1;               // in the mask box
+  // my node (i0-1+tx, j0-1+ty); it is an output ("mine") inside the owned 30 x 6 block
+  const int gi = i0 - 1 + tx, gj = j0 - 1 + ty;
+  const bool mine = tx >= 1 && tx <= OX && ty >= 1 && ty <= OY && gi <= g.nx && gj <= g.ny;
+  const int g_node = 3 * gi + rowd * gj;                 // + planed * plane
+  const int uo = (ty - 1) * OWN_W + 3 * (tx - 1);
+  const int fv = ty * VB_W + org.ov + 3 * tx;
+  const int fd = ty * DB_W + org.od + tx;
+  const int fm = ty * MB_W + org.om + tx;
+  const int fe = (ty - 1) * E_W + org.oe + tx;          // element (tx, ty), ty >= 1
 
-  auto body = [&](int it, double (&Fc)[12], double (&Fn)[12], double (&Gp)[12],
-                  double (&Gn)[12]) {
-    const int s = it % NS;
+  // my node in the previous plane: p and z (PCG) or raw u (APPLY), D^-1, fixed bits
+  double pv[3] = {0.0, 0.0, 0.0}, pz[3] = {0.0, 0.0, 0.0}, pdi = 0.0;
+  unsigned pm = 0;
+
+  for (int it = 0; it < nit; ++it, ++git) {
+    const int s = git % NS;
     double* stg = stages + s * STAGE;
-    const unsigned char* MK = reinterpret_cast<const unsigned char*>(stg + MK_OFF);
-    mbar_wait(&bars[s], (unsigned)(it / NS) & 1u);
+    double* XEn = XE + (it & 1) * 6 * NT;        // this plane's x-edges
+    double* XEp = XE + ((it & 1) ^ 1) * 6 * NT;  // previous plane's x-edges
+    mbar_wait(&bars[s], (unsigned)(git / NS) & 1u);
     const int kn = kbeg - 1 + it;  // node plane of this step
-    const bool own_plane = kn >= kbeg && kn < kend;
-    // ---- stage -> U: p = D^-1 r + beta p_old (PCG) or masked u (APPLY)
-#pragma unroll
-    for (int q = 0; q < (IN_N + NT - 1) / NT; ++q) {
-      const int f = t + q * NT;
-      if (f < IN_N) {
-        const int jj = f / IN_W;
-        const int x = f - jj * IN_W;
-        const int ii = x / 3;
-        const int c = x - 3 * ii;
-        const bool fixed = (MK[jj * MB_W + org.om + ii] >> c) & 1u;
-        const int fv = jj * VB_W + org.ov + x;
-        double v;
-        if (MODE == OP_PCG) {
-          const double po = stg[PO_OFF + fv];
-          v = fixed ? 0.0 : fma(stg[DI_OFF + jj * DB_W + org.od + ii], stg[R_OFF + fv], beta * po);
-          if (own_plane && jj >= 1 && jj <= OY && ii >= 1 && ii <= OX) {
-            const int gi = i0 - 1 + ii, gj = j0 - 1 + jj;
-            if (gi <= g.nx && gj <= g.ny) {
-              const long long gidx = 3LL * (i0 - 1) + x + rowd * gj + planed * kn;
-              a.pnew[gidx] = v;
-              a.u[gidx] = fma(alpha_prev, po, stg[UO_OFF + (jj - 1) * OWN_W + (x - 3)]);
-            }
-          }
-        } else {
-          v = fixed ? 0.0 : stg[R_OFF + fv];
-        }
-        U[f] = v;
-      }
-    }
-    const double Ecur = colv ? stg[EE_OFF + ty * E_W + org.oe + tx] : 0.0;
-    unsigned mown_next = 0;
-    double raw_next[3] = {0.0, 0.0, 0.0};
-    if (tx < OX && ty < OY) {
-      mown_next = MK[m_own];
-      if (MODE == OP_APPLY) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) raw_next[c] = stg[R_OFF + v_own + c];
-      }
-    }
-    __syncthreads();  // U complete; stage s consumed
-    if (t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
-
-    double y11[3] = {0.0, 0.0, 0.0};
-    if (colv) {
-      const double* r0 = U + ty * IN_W + tx * 3;
-      const double* r1 = r0 + IN_W;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) face_from(r0[c], r0[3 + c], r1[c], r1[3 + c], Fn, c);
-      if (it >= 1) {
-        double Gb[12];
-        element_core(Fc, Fn, Ecur, a.w, Gb, Gn);
-        if (it >= 2) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const double m00 = Gp[0 + c] + Gb[0 + c];
-            const double m10 = Gp[3 + c] + Gb[3 + c];
-            const double m01 = Gp[6 + c] + Gb[6 + c];
-            const double m11 = Gp[9 + c] + Gb[9 + c];
-            const double A_ = m00 - m01, B_ = m10 - m11, C_ = m00 + m01, D_ = m10 + m11;
-            S[(0 + c) * NT + t] = A_ - B_;  // y00
-            S[(3 + c) * NT + t] = C_ - D_;  // y01
-            S[(6 + c) * NT + t] = A_ + B_;  // y10
-            y11[c] = C_ + D_;
-          }
-        }
-      }
-    }
-    double own_next[3];
+    // ---- commit my node: p = D^-1 r + beta p_old, r = r_old - alpha q_old (PCG)
+    const unsigned m = reinterpret_cast<const unsigned char*>(stg + MK_OFF)[fm];
+    double nv[3], nz[3], ndi = 0.0;
     if (MODE == OP_PCG) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) own_next[c] = (tx < OX && ty < OY) ? U[f_own + c] : 0.0;
-    } else {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) own_next[c] = raw_next[c];
-    }
-    __syncthreads();  // S complete
-    if (it >= 2 && outv) {
-      const int ko = kn - 1;  // output node plane
-      const long long gbase = 3LL * (i0 + tx) + rowd * (j0 + ty) + planed * ko;
+      const bool wr = mine && kn >= kbeg && kn < kend;
+      ndi = stg[DI_OFF + fd];
+      const int go = g_node + planed * kn;
+      double rz = 0.0, rr = 0.0;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        double qv = y11[c] + S[(3 + c) * NT + t + 1] + S[(6 + c) * NT + t + TX] +
-                    S[(0 + c) * NT + t + TX + 1];
-        const bool fixed = (mown >> c) & 1u;
+        const bool fx = (m >> c) & 1u;
+        const double po = stg[PO_OFF + fv + c];
+        const double rn = fx ? 0.0 : fma(-alpha_prev, stg[QO_OFF + fv + c], stg[R_OFF + fv + c]);
+        nz[c] = ndi * rn;
+        nv[c] = fx ? 0.0 : fma(beta, po, nz[c]);
+        if (wr) {
+          a.rnew[go + c] = rn;
+          a.pnew[go + c] = nv[c];
+          a.u[go + c] = fma(alpha_prev, po, stg[UO_OFF + uo + c]);
+          rz = fma(nz[c], rn, rz);
+          rr = fma(rn, rn, rr);
+        }
+      }
+      if (wr) {
+        ACC[1 * NT + t] += rz;
+        ACC[2 * NT + t] += rr;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        nz[c] = stg[R_OFF + fv + c];  // raw u (identity rows at fixed DOFs)
+        nv[c] = ((m >> c) & 1u) ? 0.0 : nz[c];
+      }
+    }
+    const double Ecur = (ty >= 1) ? stg[EE_OFF + fe] : 0.0;  // lane 31: unused column
+    // ---- x-edges of my node row (partner: lane + 1)
+    double xs[3], xd[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double an = __shfl_down_sync(0xffffffffu, nv[c], 1);
+      xs[c] = nv[c] + an;
+      xd[c] = an - nv[c];
+      XEn[c * NT + t] = xs[c];
+      XEn[(3 + c) * NT + t] = xd[c];
+    }
+    __syncthreads();  // XE complete; stage s consumed
+    if (t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
+    // (a segment's last NS steps issue nothing, so the next segment starts with free stages)
+
+    double cup[3] = {0.0, 0.0, 0.0};
+    if (ty >= 1 && it >= 1) {  // warp-uniform: element row ty between node rows ty-1 and ty
+      double Fc[12], Fn[12];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double s0 = XEn[c * NT + t - TX], d0 = XEn[(3 + c) * NT + t - TX];
+        Fn[0 + c] = s0 + xs[c];
+        Fn[3 + c] = d0 + xd[c];
+        Fn[6 + c] = xs[c] - s0;
+        Fn[9 + c] = xd[c] - d0;
+        const double s1 = XEp[c * NT + t], d1 = XEp[(3 + c) * NT + t];
+        const double s0p = XEp[c * NT + t - TX], d0p = XEp[(3 + c) * NT + t - TX];
+        Fc[0 + c] = s0p + s1;
+        Fc[3 + c] = d0p + d1;
+        Fc[6 + c] = s1 - s0p;
+        Fc[9 + c] = d1 - d0p;
+      }
+      double Gb[12], Gt[12];
+      element_core(Fc, Fn, Ecur, a.w, Gb, Gt);
+      if (it >= 2) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double m00 = GS[(0 + c) * NT + t] + Gb[0 + c];
+          const double m10 = GS[(3 + c) * NT + t] + Gb[3 + c];
+          const double m01 = GS[(6 + c) * NT + t] + Gb[6 + c];
+          const double m11 = GS[(9 + c) * NT + t] + Gb[9 + c];
+          const double A_ = m00 - m01, B_ = m10 - m11, C_ = m00 + m01, D_ = m10 + m11;
+          const double y00 = A_ - B_, y10 = A_ + B_, y01 = C_ - D_, y11 = C_ + D_;
+          cup[c] = y01 + __shfl_up_sync(0xffffffffu, y11, 1);
+          CD[c * NT + t] = y00 + __shfl_up_sync(0xffffffffu, y10, 1);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 12; ++i) GS[i * NT + t] = Gt[i];
+    }
+    __syncthreads();  // CD complete
+    if (it >= 2 && mine) {
+      const int gb = g_node + planed * (kn - 1);  // output node plane kn - 1
+      double pq = 0.0, zq = 0.0, qdq = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double qv = cup[c] + CD[c * NT + t + TX];
+        const bool fixed = (pm >> c) & 1u;
         if (MODE == OP_PCG) {
           qv = fixed ? 0.0 : qv;
-          a.out[gbase + c] = qv;
-          pq = fma(own[c], qv, pq);
+          a.out[gb + c] = qv;
+          pq = fma(pv[c], qv, pq);
+          zq = fma(pz[c], qv, zq);
+          qdq = fma(pdi * qv, qv, qdq);
         } else {
-          a.out[gbase + c] = fixed ? own[c] : qv;
+          a.out[gb + c] = fixed ? pz[c] : qv;
         }
+      }
+      if (MODE == OP_PCG) {
+        ACC[0 * NT + t] += pq;
+        ACC[3 * NT + t] += zq;
+        ACC[4 * NT + t] += qdq;
       }
     }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) own[c] = own_next[c];
-    mown = mown_next;
-  };
-
-  int it = 0;
-  for (; it + 1 < nit; it += 2) {
-    body(it, F0, F1, G0, G1);
-    body(it + 1, F1, F0, G1, G0);
+    for (int c = 0; c < 3; ++c) { pv[c] = nv[c]; pz[c] = nz[c]; }
+    pdi = ndi;
+    pm = m;
   }
-  if (it < nit) body(it, F0, F1, G0, G1);
+  __syncthreads();  // segment done: XE / GS / stages may be reused by the next segment
+  }
 
   if (MODE == OP_PCG) {
-    const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
-    const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const double bs = block_sum(pq, red);
-    if (t == 0) a.partials[b] = bs;
+    const unsigned nb = gridDim.x;
+    const unsigned b = blockIdx.x;
+    double acc[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) acc[q] = ACC[q * NT + t];
+    block_sum5(acc, red);
+    if (t < 5) a.partials[5 * b + t] = acc[t];
     if (arrive_last(&a.s->cntA, nb, s_flag)) {
-      const double tot = sum_partials(a.partials, nb, 1, 0, red);
+      double tot[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      for (unsigned i = t; i < nb; i += NT) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) tot[q] += __ldcg(a.partials + 5 * (size_t)i + q);
+      }
+      block_sum5(tot, red);
       if (t == 0) {
         Scal* s = a.s;
-        s->pq = tot;
-        if (!(tot > 0.0) || !isfinite(tot)) {
-          s->status = isnan(tot) ? -6 : -4;  // TOMO_ENAN / TOMO_EBREAKDOWN
+        const int k = s->k;
+        const double pq = tot[0], rz = tot[1], rr = tot[2], zq = tot[3], qdq = tot[4];
+        s->pq = pq;
+        s->rz = rz;
+        s->rr = rr;
+        if (!isfinite(pq) || !isfinite(rz) || !isfinite(rr) || !isfinite(zq) || !isfinite(qdq)) {
+          s->status = -6;  // TOMO_ENAN
           s->done = 3;
+          s->iters = k;
+        } else if (sqrt(rr) <= s->tol_fnorm) {
+          s->done = 1;  // r_k converged: u_k (written by this launch) is the solution
+          s->iters = k;
+        } else if (k >= s->max_iters) {
+          s->done = 2;
+          s->iters = k;
+        } else if (!(pq > 0.0)) {
+          s->status = -4;  // TOMO_EBREAKDOWN
+          s->done = 3;
+          s->iters = k;
         } else {
-          s->alpha = s->rz / tot;
+          // r_{k+1}^T z_{k+1} = r.z - 2 alpha z.q + alpha^2 q.D^-1.q (exact algebra; the
+          // next launch recomputes r.z from the explicit r_{k+1}, so nothing accumulates)
+          const double alpha = rz / pq;
+          const double rz_next = fma(alpha * alpha, qdq, fma(-2.0 * alpha, zq, rz));
+          s->alpha = alpha;
+          s->beta = rz_next / rz;
+          s->k = k + 1;
         }
         s->cntA = 0;
         __threadfence();
@@ -464,80 +551,26 @@ __global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) 
 }
 
 // ------------------------------------------------------------------ K_B and reductions
-// Flat over the padded vectors (pad entries of r and q are 0).
-// mode 0: init (r holds f - K u0): rr0, rz, convergence at k = 0
-// mode 1: iteration: r -= alpha q, beta = rz_new / rz, iters += 1, convergence
-// mode 2: true residual (r holds f - K u): rr_true
-__global__ void __launch_bounds__(256) k_pcg_b(Grid g, double* __restrict__ r,
-                                               const double* __restrict__ q,
-                                               const double* __restrict__ dinv, Scal* s,
-                                               double* partials, int mode) {
+// ||r||^2 over a padded vector (pad entries are 0): the true residual at exit.
+__global__ void __launch_bounds__(256) k_norm2(Grid g, const double* __restrict__ r, Scal* s,
+                                               double* partials) {
   __shared__ double red[32];
   __shared__ int s_flag;
-  if (mode == 1 && *(volatile int*)&s->done) return;
-  const double alpha = (mode == 1) ? *(volatile double*)&s->alpha : 0.0;
-  double rr = 0.0, rz = 0.0;
-  const int n2 = (int)(g.ndof_pad / 2);  // ndof_pad is even
+  double rr = 0.0;
+  const int n2 = (int)(g.ndof_pad / 2);
   const int stride = gridDim.x * blockDim.x;
-  double2* r2 = reinterpret_cast<double2*>(r);
-  const double2* q2 = reinterpret_cast<const double2*>(q);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += 2 * stride) {
-    const int i1 = i + stride;
-    const bool has1 = i1 < n2;
-    double2 ra = r2[i], rb = has1 ? r2[i1] : make_double2(0.0, 0.0);
-    double da0 = __ldg(dinv + (2 * i) / 3), da1 = __ldg(dinv + (2 * i + 1) / 3);
-    double db0 = has1 ? __ldg(dinv + (2 * i1) / 3) : 0.0;
-    double db1 = has1 ? __ldg(dinv + (2 * i1 + 1) / 3) : 0.0;
-    if (mode == 1) {
-      const double2 qa = q2[i];
-      const double2 qb = has1 ? q2[i1] : make_double2(0.0, 0.0);
-      ra.x = fma(-alpha, qa.x, ra.x);
-      ra.y = fma(-alpha, qa.y, ra.y);
-      rb.x = fma(-alpha, qb.x, rb.x);
-      rb.y = fma(-alpha, qb.y, rb.y);
-      r2[i] = ra;
-      if (has1) r2[i1] = rb;
-    }
-    rr = fma(ra.x, ra.x, rr);
-    rz = fma(da0 * ra.x, ra.x, rz);
-    rr = fma(ra.y, ra.y, rr);
-    rz = fma(da1 * ra.y, ra.y, rz);
-    rr = fma(rb.x, rb.x, rr);
-    rz = fma(db0 * rb.x, rb.x, rz);
-    rr = fma(rb.y, rb.y, rr);
-    rz = fma(db1 * rb.y, rb.y, rz);
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const double2 v = r2[i];
+    rr = fma(v.x, v.x, rr);
+    rr = fma(v.y, v.y, rr);
   }
-  const double brr = block_sum(rr, red);
-  const double brz = block_sum(rz, red);
-  if (threadIdx.x == 0) {
-    partials[2 * blockIdx.x] = brr;
-    partials[2 * blockIdx.x + 1] = brz;
-  }
+  const double b = block_sum(rr, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
   if (arrive_last(&s->cntB, gridDim.x, &s_flag)) {
-    const double trr = sum_partials(partials, gridDim.x, 2, 0, red);
-    const double trz = sum_partials(partials, gridDim.x, 2, 1, red);
+    const double tot = sum_partials(partials, gridDim.x, 1, 0, red);
     if (threadIdx.x == 0) {
-      if (mode == 2) {
-        s->rr_true = trr;
-      } else if (!isfinite(trr) || !isfinite(trz)) {
-        s->status = -6;
-        s->done = 3;
-      } else if (mode == 0) {
-        s->rr0 = trr;
-        s->rr = trr;
-        s->rz = trz;
-        s->beta = 0.0;
-        s->alpha = 0.0;
-        s->iters = 0;
-        if (sqrt(trr) <= s->tol_fnorm) s->done = 1;
-      } else {
-        s->beta = trz / s->rz;
-        s->rz = trz;
-        s->rr = trr;
-        s->iters += 1;
-        if (sqrt(trr) <= s->tol_fnorm) s->done = 1;
-        else if (s->iters >= s->max_iters) s->done = 2;
-      }
+      s->rr_true = tot;
       s->cntB = 0;
       __threadfence();
     }
@@ -546,9 +579,9 @@ __global__ void __launch_bounds__(256) k_pcg_b(Grid g, double* __restrict__ r,
 
 __global__ void k_scal_init(Scal* s, double tol_fnorm, int max_iters) {
   s->alpha = 0.0; s->beta = 0.0; s->rz = 0.0; s->rr = 0.0; s->pq = 0.0;
-  s->rr0 = 0.0; s->rr_true = 0.0; s->tol_fnorm = tol_fnorm; s->energy = 0.0; s->comp = 0.0;
-  s->iters = 0; s->done = 0; s->status = 0; s->max_iters = max_iters; s->domain_bad = 0;
-  s->cntA = 0; s->cntB = 0; s->cntR = 0;
+  s->rr_true = 0.0; s->tol_fnorm = tol_fnorm; s->energy = 0.0; s->comp = 0.0;
+  s->k = 0; s->iters = 0; s->done = 0; s->status = 0; s->max_iters = max_iters;
+  s->domain_bad = 0; s->cntA = 0; s->cntB = 0; s->cntR = 0;
 }
 
 // r = -q (padded), then r[load dof] += f (loads are distinct DOFs)
@@ -560,19 +593,6 @@ __global__ void k_resid(long long n, const double* __restrict__ q, double* __res
 __global__ void k_add_loads(double* r, const int64_t* dofs, const double* vals, int n) {
   for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < n; i += blockDim.x * gridDim.x)
     r[dofs[i]] += vals[i];
-}
-
-// deferred last update u += alpha_k p_k (p_k is in p[iters & 1]); fixed entries stay 0
-__global__ void k_finish(long long n, double* __restrict__ u, const double* __restrict__ p0,
-                         const double* __restrict__ p1, const Scal* s) {
-  const int done = s->done;
-  const int it = s->iters;
-  if (!(done == 1 || done == 2) || it == 0) return;
-  const double alpha = s->alpha;
-  const double* p = (it & 1) ? p1 : p0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride)
-    u[d] = fma(alpha, p[d], u[d]);
 }
 
 // dense ABI vector -> padded internal vector, fixed entries zeroed
@@ -863,13 +883,12 @@ inline unsigned nblk(long long n, int bs, int cap) {
 }  // namespace
 
 // ================================================================== launch helpers
-dim3 op_grid(const Grid& g, int nchunk) {
-  return dim3((unsigned)((g.nnx + OX - 1) / OX), (unsigned)((g.nny + OY - 1) / OY),
-              (unsigned)nchunk);
+int op_tiles(const Grid& g) {
+  return ((g.nnx + OX - 1) / OX) * ((g.nny + OY - 1) / OY);
 }
 
 size_t op_smem(int /*mode*/) {
-  return sizeof(double) * ((size_t)NS * STAGE + IN_N + 9 * NT + 32) + sizeof(uint64_t) * NS + 16;
+  return sizeof(double) * ((size_t)NS * STAGE + 32 * NT + 168) + sizeof(uint64_t) * NS + 16;
 }
 
 static void op_attr() {
@@ -881,10 +900,10 @@ static void op_attr() {
   done = true;
 }
 
-cudaError_t launch_op(int mode, const OpArgs& a, dim3 grid, cudaStream_t st) {
+cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st) {
   op_attr();
-  if (mode == OP_PCG) k_op<OP_PCG><<<grid, dim3(TX, BY), op_smem(1), st>>>(a);
-  else k_op<OP_APPLY><<<grid, dim3(TX, BY), op_smem(0), st>>>(a);
+  if (mode == OP_PCG) k_op<OP_PCG><<<nblocks, dim3(TX, BY), op_smem(1), st>>>(a);
+  else k_op<OP_APPLY><<<nblocks, dim3(TX, BY), op_smem(0), st>>>(a);
   return cudaGetLastError();
 }
 
@@ -927,14 +946,9 @@ cudaError_t launch_resid(const Grid& g, const double* q, double* r, const int64_
   if (nloads > 0) k_add_loads<<<nblk(nloads, 256, 64), 256, 0, st>>>(r, ldofs, lvals, nloads);
   return cudaGetLastError();
 }
-cudaError_t launch_pcg_b(const Grid& g, double* r, const double* q, const double* dinv,
-                         Scal* s, double* partials, int nblocks, int mode, cudaStream_t st) {
-  k_pcg_b<<<nblocks, 256, 0, st>>>(g, r, q, dinv, s, partials, mode);
-  return cudaGetLastError();
-}
-cudaError_t launch_finish(const Grid& g, double* u, const double* p0, const double* p1, Scal* s,
-                          cudaStream_t st) {
-  k_finish<<<nblk(g.ndof_pad, 256, 148 * 16), 256, 0, st>>>(g.ndof_pad, u, p0, p1, s);
+cudaError_t launch_norm2(const Grid& g, const double* r, Scal* s, double* partials,
+                         int nblocks, cudaStream_t st) {
+  k_norm2<<<nblocks, 256, 0, st>>>(g, r, s, partials);
   return cudaGetLastError();
 }
 cudaError_t launch_compliance(const double* u, const int64_t* ldofs, const double* lvals,

@@ -46,19 +46,21 @@ struct Walsh {
 };
 
 // Device-side scalar state of one PCG solve (read/written only by kernels, except the
-// host reads it back once per batch of iterations).
+// host reads it back once per batch of iterations). Single-pass PCG:
+// launch k forms r_k = r_{k-1} - alpha_{k-1} q_{k-1}, p_k = D^-1 r_k + beta_{k-1} p_{k-1},
+// u_k = u_{k-1} + alpha_{k-1} p_{k-1}, q_k = K p_k and reduces p.q, r.z, r.r, z.q, q.D^-1 q.
 struct Scal {
-  double alpha;       // alpha of the latest K_A (also the deferred u update factor)
-  double beta;        // beta for the next K_A
-  double rz;          // r^T D^-1 r of the current residual
-  double rr;          // r^T r of the current residual (recursive)
-  double pq;          // p^T K p of the latest iteration
-  double rr0;         // r0^T r0
+  double alpha;       // alpha_{k-1} for the next launch
+  double beta;        // beta_{k-1} for the next launch
+  double rz;          // r_k^T D^-1 r_k (exact, from the explicit r_k)
+  double rr;          // r_k^T r_k
+  double pq;          // p_k^T K p_k
   double rr_true;     // ||f - K u||^2 at exit
   double tol_fnorm;   // tol * ||f||
   double energy;      // sum_e E_e ce_e (sensitivity)
   double comp;        // f^T u
-  int iters;          // completed iterations
+  int k;              // index of the next PCG launch
+  int iters;          // products that contributed to u (standard PCG count)
   int done;           // 0 running, 1 converged, 2 max_iters, 3 error
   int status;         // tomo_status of an error
   int max_iters;
@@ -69,36 +71,40 @@ struct Scal {
 
 enum OpMode { OP_APPLY = 0, OP_PCG = 1 };
 
-// Operator tile: 32 x OP_BY threads; thread (tx, ty) owns element column
-// (i0-1+tx, j0-1+ty) for tx < 31, and output node (i0+tx, j0+ty) for tx < OP_OX,
-// ty < OP_OY. A block marches along z through a chunk of node planes.
+// Operator tile: 32 x OP_BY threads. Warp ty stages node row j0-1+ty (OP_BY node rows);
+// thread (tx, ty >= 1) computes element column (i0-1+tx, j0-2+ty) (OP_BY-1 element rows);
+// thread (tx, ty) outputs node (i0-1+tx, j0-1+ty) for 1 <= tx <= OP_OX, 1 <= ty <= OP_OY.
+// x-neighbours are exchanged with warp shuffles, y-neighbours through shared memory.
+// A block marches along z through a chunk of node planes.
 constexpr int OP_BY = 8;
 constexpr int OP_OX = 30;           // output nodes per tile along x (even: 16-B TMA rows)
-constexpr int OP_OY = OP_BY - 1;    // output nodes per tile along y
-constexpr int OP_NS = 3;            // TMA pipeline stages (node planes in flight)
+constexpr int OP_OY = OP_BY - 2;    // output nodes per tile along y
+constexpr int OP_NS = 1;            // TMA stages: plane k+1 loads during plane k's compute
 
 struct OpArgs {
-  CUtensorMap tm_in;    // APPLY: u ; PCG: r   (box 96 x (BY+1) doubles)
-  CUtensorMap tm_pold;  // PCG: p_{k-1}        (box 96 x (BY+1))
+  CUtensorMap tm_in;    // APPLY: u ; PCG: r_{k-1} (box 98 x (BY+1) doubles)
+  CUtensorMap tm_qold;  // PCG: q_{k-1}            (box 98 x (BY+1))
+  CUtensorMap tm_pold;  // PCG: p_{k-1}            (box 98 x (BY+1))
   CUtensorMap tm_uown;  // PCG: u, owned box   (box 90 x BY-1)
   CUtensorMap tm_dinv;  // PCG: Jacobi, per node (box 32 x (BY+1))
   CUtensorMap tm_mask;  // fixed mask bytes     (box 32 x (BY+1))
   CUtensorMap tm_E;     // element modulus      (box 32 x BY)
   Grid g;
   Walsh w;
+  double* rnew;         // PCG: r_k (owned nodes written)
   double* pnew;         // PCG: p_k (owned nodes written)
   double* u;            // PCG: u (owned nodes: u += alpha_{k-1} p_{k-1})
   double* out;          // APPLY: y (raw u at fixed DOFs) ; PCG: q
-  double* partials;     // PCG: one per block
+  double* partials;     // PCG: five per block
   Scal* s;              // PCG
-  int nchunk;           // z chunks (gridDim.z)
+  int ntiles;           // x-y tiles; the grid is persistent (1-D, balanced)
 };
 
 // launch helpers (kernels.cu). All enqueue on `st`; return the launch error.
-dim3 op_grid(const Grid& g, int nchunk);
+int op_tiles(const Grid& g);
 size_t op_smem(int mode);
 int op_occupancy(int mode);
-cudaError_t launch_op(int mode, const OpArgs& a, dim3 grid, cudaStream_t st);
+cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_simp(const Grid& g, const double* rho, double* E, double E0, double Emin,
                         double penal, Scal* s, cudaStream_t st);
 cudaError_t launch_jacobi(const Grid& g, const double* E, double ke_diag, double* dinv,
@@ -111,10 +117,8 @@ cudaError_t launch_scal_init(Scal* s, double tol_fnorm, int max_iters, cudaStrea
 // r = -q + f (sparse f at padded DOF indices)
 cudaError_t launch_resid(const Grid& g, const double* q, double* r, const int64_t* ldofs_pad,
                          const double* lvals, int nloads, cudaStream_t st);
-cudaError_t launch_pcg_b(const Grid& g, double* r, const double* q, const double* dinv,
-                         Scal* s, double* partials, int nblocks, int mode, cudaStream_t st);
-cudaError_t launch_finish(const Grid& g, double* u, const double* p0, const double* p1, Scal* s,
-                          cudaStream_t st);
+cudaError_t launch_norm2(const Grid& g, const double* r, Scal* s, double* partials,
+                         int nblocks, cudaStream_t st);
 cudaError_t launch_compliance(const double* u, const int64_t* ldofs, const double* lvals,
                               int nloads, Scal* s, cudaStream_t st);
 cudaError_t launch_sens(const Grid& g, const Walsh& w, const double* rho, const double* u,
