@@ -313,8 +313,7 @@ __global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) 
   double* XE = stages + NS * STAGE;          // [2][6][NT] x-edge sums / differences (by plane parity)
   double* CD = XE + 12 * NT;                 // [3][NT] row-ty contributions to row ty-1
   double* GS = CD + 3 * NT;                  // [12][NT] thread-private: top-face sums of the last element
-  double* ACC = GS + 12 * NT;                // [5][NT] thread-private reduction accumulators
-  double* red = ACC + 5 * NT;                // [168]
+  double* red = GS + 12 * NT;                // [168]
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 168);  // [NS]
   int* s_flag = reinterpret_cast<int*>(bars + NS);
 
@@ -342,9 +341,8 @@ __global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) 
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-#pragma unroll
-  for (int q = 0; q < 5; ++q) ACC[q * NT + t] = 0.0;
   __syncthreads();
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // p.q, r.z, r.r, z.q, q.D^-1.q
 
   int git = 0;  // global step counter (mbarrier phase)
   for (int u0 = ub; u0 < ue;) {
@@ -405,10 +403,8 @@ __global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) 
           rr = fma(rn, rn, rr);
         }
       }
-      if (wr) {
-        ACC[1 * NT + t] += rz;
-        ACC[2 * NT + t] += rr;
-      }
+      acc[1] += rz;
+      acc[2] += rr;
     } else {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -484,11 +480,9 @@ __global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) 
           a.out[gb + c] = fixed ? pz[c] : qv;
         }
       }
-      if (MODE == OP_PCG) {
-        ACC[0 * NT + t] += pq;
-        ACC[3 * NT + t] += zq;
-        ACC[4 * NT + t] += qdq;
-      }
+      acc[0] += pq;
+      acc[3] += zq;
+      acc[4] += qdq;
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) { pv[c] = nv[c]; pz[c] = nz[c]; }
@@ -501,9 +495,6 @@ __global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) 
   if (MODE == OP_PCG) {
     const unsigned nb = gridDim.x;
     const unsigned b = blockIdx.x;
-    double acc[5];
-#pragma unroll
-    for (int q = 0; q < 5; ++q) acc[q] = ACC[q * NT + t];
     block_sum5(acc, red);
     if (t < 5) a.partials[5 * b + t] = acc[t];
     if (arrive_last(&a.s->cntA, nb, s_flag)) {
@@ -888,7 +879,7 @@ int op_tiles(const Grid& g) {
 }
 
 size_t op_smem(int /*mode*/) {
-  return sizeof(double) * ((size_t)NS * STAGE + 32 * NT + 168) + sizeof(uint64_t) * NS + 16;
+  return sizeof(double) * ((size_t)NS * STAGE + 27 * NT + 168) + sizeof(uint64_t) * NS + 16;
 }
 
 static void op_attr() {

@@ -79,7 +79,7 @@ enum OpMode { OP_APPLY = 0, OP_PCG = 1 };
 constexpr int OP_BY = 8;
 constexpr int OP_OX = 30;           // output nodes per tile along x (even: 16-B TMA rows)
 constexpr int OP_OY = OP_BY - 2;    // output nodes per tile along y
-constexpr int OP_NS = 1;            // TMA stages: plane k+1 loads during plane k's compute
+constexpr int OP_NS = 2;            // TMA pipeline stages (node planes in flight)
 
 struct OpArgs {
   CUtensorMap tm_in;    // APPLY: u ; PCG: r_{k-1} (box 98 x (BY+1) doubles)
