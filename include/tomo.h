@@ -185,9 +185,13 @@ int64_t tomo_launch_count(const tomo_ctx* ctx);
  * sustained FP64 FMA rate (GFLOP/s, FMA = 2 flop) and the per-launch mean time of the
  * PCG kernels of the last tomo_solve measured with CUDA events on the bound stream.      */
 int tomo_bench_dfma(tomo_ctx* ctx, double* gflops_out, double* ms_out);
-/* times[0] = K_A (fused operator) mean ms per launch, times[1] = K_B mean ms, times[2] =
- * number of K_A launches timed. Requires tomo_set_profiling(ctx, 1) before the solve.   */
+/* times[0] = mean ms per fused PCG launch, times[1] = 0 (no separate K_B kernel), times[2]
+ * = number of launches timed. Requires tomo_set_profiling(ctx, 1) before the solve.      */
 int tomo_set_profiling(tomo_ctx* ctx, int on);
+/* K_hat u throughput: E from d_rho, then `reps` back-to-back launches of the operator
+ * kernel on the workspace's internal (padded) u, timed with CUDA events on the bound stream;
+ * *ms_out = mean ms per application.                                                    */
+int tomo_bench_apply(tomo_ctx* ctx, const double* d_rho, int reps, double* ms_out);
 int tomo_profile_times(const tomo_ctx* ctx, double* times3);
 
 #ifdef __cplusplus

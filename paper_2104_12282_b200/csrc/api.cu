@@ -861,3 +861,23 @@ extern "C" int tomo_profile_times(const tomo_ctx* c, double* t) {
   t[2] = (double)c->prof_n;
   return TOMO_OK;
 }
+
+extern "C" int tomo_bench_apply(tomo_ctx* c, const double* d_rho, int reps, double* ms_out) {
+  if (int rc = need_bound(c)) return rc;
+  if (!check_ptr(d_rho) || reps < 1) return fail(c, TOMO_EINVAL, "bad argument");
+  if (int rc = prepare_modulus(c, d_rho, false)) return rc;
+  cudaEvent_t e0, e1;
+  CK(c, cudaEventCreate(&e0));
+  CK(c, cudaEventCreate(&e1));
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));  // warm-up
+  CK(c, cudaEventRecord(e0, c->st));
+  for (int i = 0; i < reps; ++i) LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));
+  CK(c, cudaEventRecord(e1, c->st));
+  CK(c, cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(c, cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (ms_out) *ms_out = ms / reps;
+  return TOMO_OK;
+}

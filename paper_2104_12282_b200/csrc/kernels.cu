@@ -623,7 +623,7 @@ __global__ void k_simp(Grid g, const double* __restrict__ rho, double* __restric
     const int j = (int)((e / g.nx) % g.ny);
     const int k = (int)(e / ((long long)g.nx * g.ny));
     const double r = rho[e];
-    bad |= !(r >= 0.0 && r <= 1.0);
+    bad |= !(r >= -1e-12 && r <= 1.0 + 1e-12);  // SPEC.md l.118 with reading R3 (rounding)
     E[elem_pad(g, i, j, k)] = Emin + pow(r, penal) * (E0 - Emin);
   }
   if (bad) s->domain_bad = 1;

@@ -93,6 +93,7 @@ _SIGS = [
     ("tomo_bench_dfma", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("tomo_set_profiling", C.c_int, [C.c_void_p, C.c_int]),
     ("tomo_profile_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    ("tomo_bench_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_double)]),
 ]
 EXPORTS = [s[0] for s in _SIGS]
 
@@ -339,6 +340,11 @@ class Tomo:
         t = (C.c_double * 3)()
         self._check(self.lib.tomo_profile_times(self.h, t))
         return {"k_a_ms": t[0], "k_b_ms": t[1], "n": int(t[2])}
+
+    def bench_apply(self, rho: torch.Tensor, reps: int = 100) -> float:
+        ms = C.c_double()
+        self._check(self.lib.tomo_bench_apply(self.h, _ptr(_f64(rho, self.n_e, "rho")), reps, C.byref(ms)))
+        return ms.value
 
 
 def params_from_problem(p) -> Params:

@@ -1,0 +1,170 @@
+"""GPU parity at the BASELINE.json configs' full sizes, in the launch configuration bench.py
+times (the same context code path). Where the oracle cannot finish a full solve in seconds
+(configs[3], [4]), the CUDA result is checked through properties the oracle computes one
+pass at a time: the true residual of u_gpu under the oracle's own K_hat, the oracle's c and
+dc evaluated at u_gpu, and operator parity."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import filt, oc as ooc, sens
+from oracle.loop import OracleProblem
+from paper_2104_12282_b200 import inputs, tomo
+from paper_2104_12282_b200.loop import SimpLoop
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gpu(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=DEV)
+
+
+def cpu(t):
+    return t.detach().cpu().numpy()
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def ctx(p):
+    return tomo.Tomo(tomo.params_from_problem(p), device=DEV)
+
+
+# ------------------------------------------------------------------ configs[3], the metric
+def test_cfg3_evaluation_residual_pins():
+    p = inputs.CFG3
+    rho = inputs.density_for("cfg3")
+    t = ctx(p)
+    u_g, c, dcf, info = t.evaluate(gpu(rho), tol=1e-10)
+    assert info.converged == 1
+    u = cpu(u_g)
+    op = OracleProblem(p, assemble=False)
+    r = op.f - op.apply(rho, u)
+    rel_true = np.linalg.norm(r) / np.linalg.norm(op.f)
+    # the GPU's own true-residual report agrees with the oracle's operator
+    assert abs(rel_true - info.rel_res_true) <= 1e-3 * rel_true + 1e-14
+    assert rel_true <= 2e-9  # high contrast (1e9): the recursive 1e-10 drifts
+    assert abs(c - sens.compliance(op.f, u)) <= 1e-12 * abs(c)
+    dc_ref, ce = op.sensitivity(rho, u)
+    dc = cpu(t.sensitivity(gpu(rho), u_g))
+    assert rel(dc, dc_ref) <= 1e-12
+    # energy identity f^T u = u^T K u up to u^T r
+    E = op.E(rho)
+    assert abs(float(np.dot(E, ce)) - c) <= 1e-8 * c
+    P = filt.filter_matrix(p.nx, p.ny, p.nz, p.rmin)
+    assert rel(cpu(dcf), filt.apply_transpose(P, dc_ref)) <= 1e-12
+
+
+# ------------------------------------------------------------------ configs[2]
+def _gold(name):
+    path = os.path.join(GOLD, f"{name}_solve.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"golden {path} missing (python scripts/make_golden.py {name})")
+    with open(os.path.join(GOLD, f"{name}_solve.json")) as f:
+        meta = json.load(f)
+    return meta, np.load(path)
+
+
+def test_cfg2_mbb_half_beam_against_tight_oracle():
+    meta, gold = _gold("cfg2")
+    p = inputs.CFG2
+    rho = inputs.density_for("cfg2")
+    t = ctx(p)
+    u_g, c, dcf, info = t.evaluate(gpu(rho), tol=1e-10)
+    assert info.converged == 1
+    assert abs(info.iterations - meta["pcg_iters_1e-10"]) <= max(3, 0.02 * meta["pcg_iters_1e-10"])
+    assert abs(c - meta["c"]) <= 1e-9 * abs(meta["c"])
+    # u and dc at 1e-10: bounded by the solver-noise floor (reading A14); at 1e-12 the bar is 1e-8
+    u12, info12 = t.solve(gpu(rho), tol=1e-12)
+    assert rel(cpu(u12), gold["u"]) <= 1e-8
+    dc12 = cpu(t.sensitivity(gpu(rho), u12))
+    assert rel(dc12, gold["dc"]) <= 1e-8
+    assert rel(cpu(dcf), gold["dcf"]) <= 1e-6
+    assert rel(cpu(u_g), gold["u"]) <= 1e-6
+
+
+def test_cfg0_against_stored_tight_oracle_if_present():
+    path = os.path.join(GOLD, "cfg0_solve.npz")
+    if not os.path.exists(path):
+        pytest.skip("cfg0 golden not generated (the direct-solve parity in test_gpu_parity covers cfg0)")
+    meta, gold = _gold("cfg0")
+    t = ctx(inputs.CFG0)
+    rho = inputs.density_for("cfg0")
+    u_g, c, dcf, info = t.evaluate(gpu(rho), tol=1e-10)
+    assert abs(c - meta["c"]) <= 1e-9 * abs(meta["c"])
+    assert rel(cpu(dcf), gold["dcf"]) <= 1e-8
+
+
+# ------------------------------------------------------------------ configs[4] sweep
+@pytest.mark.parametrize("idx", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", ["void07", "uniform"])
+def test_cfg4_operator_parity(idx, variant):
+    p = inputs.cfg4(idx)
+    if p.n_elem > 2_000_000 and variant == "uniform":
+        pytest.skip("largest grid checked once (void07) to bound the oracle's host memory")
+    rho = inputs.density_void07(p) if variant == "void07" else inputs.density_uniform(p, 0.5)
+    op = OracleProblem(p, assemble=False)
+    u = inputs.random_vector(op.n_dof, seed=idx + 40)
+    t = ctx(p)
+    y = cpu(t.apply(gpu(rho), gpu(u)))
+    assert rel(y, op.apply(rho, u)) <= 1e-13
+
+
+def test_cfg4a_solve_residual_pins():
+    p = inputs.cfg4(0)
+    rho = inputs.density_void07(p)
+    t = ctx(p)
+    u_g, info = t.solve(gpu(rho), tol=1e-10)
+    assert info.converged == 1
+    op = OracleProblem(p)
+    u = cpu(u_g)
+    r = op.f - op.Khat(rho) @ u
+    assert abs(np.linalg.norm(r) / np.linalg.norm(op.f) - info.rel_res_true) <= 1e-3 * info.rel_res_true
+    # the oracle's own PCG from x0 = 0 takes (nearly) the same number of iterations
+    _, its, conv, _ = op.solve_pcg(rho, tol=1e-10)
+    assert conv and abs(its - info.iterations) <= max(3, 0.02 * its)
+
+
+# ------------------------------------------------------------------ configs[1]: 50-step loop
+def _loop_gold():
+    jp = os.path.join(GOLD, "cfg1_loop.json")
+    if not os.path.exists(jp):
+        pytest.fail("golden cfg1_loop.json missing (python scripts/make_golden.py cfg1)")
+    with open(jp) as f:
+        h = json.load(f)
+    return h, np.load(os.path.join(GOLD, "cfg1_x.npz"))
+
+
+def test_cfg1_loop_teacher_forced():
+    h, xs = _loop_gold()
+    p = inputs.CFG1
+    t = ctx(p)
+    loop = SimpLoop(t, volfrac=p.volfrac, move=p.move, eta=p.eta, tol=1e-10)
+    for k in (0, 1, 10, 25, 49):
+        xn, c, lam, steps, info = loop.step(gpu(xs[f"x{k}"]))
+        assert abs(c - h["c"][k]) <= 1e-9 * h["c"][k], k
+        assert abs(lam - h["lam"][k]) <= 1e-8 * h["lam"][k], k
+        nxt = f"x{k + 1}"
+        if nxt in xs:
+            assert np.max(np.abs(cpu(xn) - xs[nxt])) <= 1e-6, k
+
+
+def test_cfg1_loop_free_running_history():
+    h, xs = _loop_gold()
+    p = inputs.CFG1
+    t = ctx(p)
+    loop = SimpLoop(t, volfrac=p.volfrac, move=p.move, eta=p.eta, tol=1e-10)
+    hist = loop.run(gpu(xs["x0"]), p.loop_iters)
+    c_ref = np.array(h["c"])
+    c = np.array(hist["c"])
+    relc = np.abs(c - c_ref) / c_ref
+    assert relc[0] <= 1e-9
+    assert np.max(relc) <= 1e-6, relc
+    assert c[-1] < c[0]  # the standard optimiser makes progress
+    assert np.max(np.abs(cpu(hist["x_final"]) - xs["x50"])) <= 1e-4
