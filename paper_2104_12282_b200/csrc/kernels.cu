@@ -47,23 +47,15 @@ constexpr int DB_W = OX + 4;           // 34 doubles: Jacobi rows (start offset 
 constexpr int MB_W = 48;               // 48 bytes: mask rows (start offset 0..15)
 constexpr int E_W = 32;                // element box width (start offset 0..1, 31 used)
 // stage layout in doubles, every piece 128-byte aligned
-constexpr int R_OFF = 0;               // r_{k-1} (APPLY: u), 784 used
-constexpr int QO_OFF = 784;            // q_{k-1}, 784 used
-constexpr int PO_OFF = 1568;           // p_{k-1}, 784 used
-constexpr int UO_OFF = 2352;           // u, owned box, 540 used
-constexpr int DI_OFF = 2896;           // D^-1, 272 used
-constexpr int EE_OFF = 3168;           // E, 224 used
-constexpr int MK_OFF = 3392;           // mask, 384 bytes used
-constexpr int STAGE = 3456;            // 27648 B
-static_assert(QO_OFF >= VB_W * NR && PO_OFF - QO_OFF >= VB_W * NR &&
-                  UO_OFF - PO_OFF >= VB_W * NR && DI_OFF - UO_OFF >= OWN_N &&
-                  EE_OFF - DI_OFF >= DB_W * NR && MK_OFF - EE_OFF >= E_W * ER &&
-                  (STAGE - MK_OFF) * 8 >= MB_W * NR,
-              "stage pieces overlap");
-static_assert((QO_OFF * 8) % 128 == 0 && (PO_OFF * 8) % 128 == 0 && (UO_OFF * 8) % 128 == 0 &&
-                  (DI_OFF * 8) % 128 == 0 && (EE_OFF * 8) % 128 == 0 && (MK_OFF * 8) % 128 == 0 &&
-                  (STAGE * 8) % 128 == 0,
-              "TMA destinations must stay 128-byte aligned");
+constexpr int al16(int n) { return (n + 15) & ~15; }  // doubles -> multiple of 128 B
+constexpr int R_OFF = 0;                                       // r_{k-1} (APPLY: u)
+constexpr int QO_OFF = R_OFF + al16(VB_W * NR);                // q_{k-1}
+constexpr int PO_OFF = QO_OFF + al16(VB_W * NR);               // p_{k-1}
+constexpr int UO_OFF = PO_OFF + al16(VB_W * NR);               // u, owned box
+constexpr int DI_OFF = UO_OFF + al16(OWN_N);                   // D^-1
+constexpr int EE_OFF = DI_OFF + al16(DB_W * NR);               // E
+constexpr int MK_OFF = EE_OFF + al16(E_W * ER);                // mask bytes
+constexpr int STAGE = MK_OFF + al16((MB_W * NR + 7) / 8);
 constexpr unsigned BYTES_PCG = 8u * (3 * VB_W * NR + OWN_N + DB_W * NR + E_W * ER) + MB_W * NR;
 constexpr unsigned BYTES_APPLY = 8u * (VB_W * NR + E_W * ER) + MB_W * NR;
 
@@ -307,13 +299,13 @@ __device__ __forceinline__ void issue_plane(const OpArgs& a, double* stg, uint64
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpArgs a) {
   extern __shared__ __align__(128) double smem[];
   double* stages = smem;                     // [NS][STAGE]
   double* XE = stages + NS * STAGE;          // [2][6][NT] x-edge sums / differences (by plane parity)
   double* CD = XE + 12 * NT;                 // [3][NT] row-ty contributions to row ty-1
-  double* GS = CD + 3 * NT;                  // [12][NT] thread-private: top-face sums of the last element
-  double* red = GS + 12 * NT;                // [168]
+  double* GS = CD + 3 * NT;                  // [6][NT] thread-private: top-face node sums of the last element
+  double* red = GS + 6 * NT;                 // [168]
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 168);  // [NS]
   int* s_flag = reinterpret_cast<int*>(bars + NS);
 
@@ -446,21 +438,28 @@ __global__ void __launch_bounds__(NT, 2) k_op(const __grid_constant__ OpArgs a) 
       }
       double Gb[12], Gt[12];
       element_core(Fc, Fn, Ecur, a.w, Gb, Gt);
-      if (it >= 2) {
+      // inverse xy transform of each face, combined along x through the warp: this
+      // element's bottom face feeds node rows (ty-1, ty) of plane kn-1 together with the
+      // top face of the element below (carried in GS as node contributions, 6 per thread)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double m00 = GS[(0 + c) * NT + t] + Gb[0 + c];
-          const double m10 = GS[(3 + c) * NT + t] + Gb[3 + c];
-          const double m01 = GS[(6 + c) * NT + t] + Gb[6 + c];
-          const double m11 = GS[(9 + c) * NT + t] + Gb[9 + c];
-          const double A_ = m00 - m01, B_ = m10 - m11, C_ = m00 + m01, D_ = m10 + m11;
+      for (int c = 0; c < 3; ++c) {
+        {  // top face -> plane kn, kept for the next step
+          const double A_ = Gt[0 + c] - Gt[6 + c], B_ = Gt[3 + c] - Gt[9 + c];
+          const double C_ = Gt[0 + c] + Gt[6 + c], D_ = Gt[3 + c] + Gt[9 + c];
           const double y00 = A_ - B_, y10 = A_ + B_, y01 = C_ - D_, y11 = C_ + D_;
-          cup[c] = y01 + __shfl_up_sync(0xffffffffu, y11, 1);
-          CD[c * NT + t] = y00 + __shfl_up_sync(0xffffffffu, y10, 1);
+          const double tup = y01 + __shfl_up_sync(0xffffffffu, y11, 1);
+          const double tdn = y00 + __shfl_up_sync(0xffffffffu, y10, 1);
+          if (it >= 2) {
+            const double A2 = Gb[0 + c] - Gb[6 + c], B2 = Gb[3 + c] - Gb[9 + c];
+            const double C2 = Gb[0 + c] + Gb[6 + c], D2 = Gb[3 + c] + Gb[9 + c];
+            const double b00 = A2 - B2, b10 = A2 + B2, b01 = C2 - D2, b11 = C2 + D2;
+            cup[c] = GS[c * NT + t] + (b01 + __shfl_up_sync(0xffffffffu, b11, 1));
+            CD[c * NT + t] = GS[(3 + c) * NT + t] + (b00 + __shfl_up_sync(0xffffffffu, b10, 1));
+          }
+          GS[c * NT + t] = tup;
+          GS[(3 + c) * NT + t] = tdn;
         }
       }
-#pragma unroll
-      for (int i = 0; i < 12; ++i) GS[i * NT + t] = Gt[i];
     }
     __syncthreads();  // CD complete
     if (it >= 2 && mine) {
@@ -879,7 +878,7 @@ int op_tiles(const Grid& g) {
 }
 
 size_t op_smem(int /*mode*/) {
-  return sizeof(double) * ((size_t)NS * STAGE + 27 * NT + 168) + sizeof(uint64_t) * NS + 16;
+  return sizeof(double) * ((size_t)NS * STAGE + 21 * NT + 168) + sizeof(uint64_t) * NS + 16;
 }
 
 static void op_attr() {

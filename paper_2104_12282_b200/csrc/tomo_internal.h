@@ -76,7 +76,11 @@ enum OpMode { OP_APPLY = 0, OP_PCG = 1 };
 // thread (tx, ty) outputs node (i0-1+tx, j0-1+ty) for 1 <= tx <= OP_OX, 1 <= ty <= OP_OY.
 // x-neighbours are exchanged with warp shuffles, y-neighbours through shared memory.
 // A block marches along z through a chunk of node planes.
-constexpr int OP_BY = 8;
+#ifndef TOMO_OP_BY
+#define TOMO_OP_BY 8
+#endif
+constexpr int OP_BY = TOMO_OP_BY;
+constexpr int OP_MINB = OP_BY >= 16 ? 1 : 2;  // resident blocks per SM the tile is sized for
 constexpr int OP_OX = 30;           // output nodes per tile along x (even: 16-B TMA rows)
 constexpr int OP_OY = OP_BY - 2;    // output nodes per tile along y
 constexpr int OP_NS = 2;            // TMA pipeline stages (node planes in flight)

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libtomo.so")
+LIB_PATH = os.environ.get("TOMO_LIB_PATH") or os.path.join(_PKG, "lib", "libtomo.so")
 
 TOMO_BC_CANTILEVER = 1
 TOMO_BC_MBB_HALF = 2
