@@ -304,8 +304,8 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
   double* stages = smem;                     // [NS][STAGE]
   double* XE = stages + NS * STAGE;          // [2][6][NT] x-edge sums / differences (by plane parity)
   double* CD = XE + 12 * NT;                 // [3][NT] row-ty contributions to row ty-1
-  double* GS = CD + 3 * NT;                  // [6][NT] thread-private: top-face node sums of the last element
-  double* red = GS + 6 * NT;                 // [168]
+  double* GS = CD + 3 * NT;                  // [12][NT] thread-private: top-face sums of the last element
+  double* red = GS + 12 * NT;                // [168]
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 168);  // [NS]
   int* s_flag = reinterpret_cast<int*>(bars + NS);
 
@@ -438,28 +438,21 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
       }
       double Gb[12], Gt[12];
       element_core(Fc, Fn, Ecur, a.w, Gb, Gt);
-      // inverse xy transform of each face, combined along x through the warp: this
-      // element's bottom face feeds node rows (ty-1, ty) of plane kn-1 together with the
-      // top face of the element below (carried in GS as node contributions, 6 per thread)
+      if (it >= 2) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        {  // top face -> plane kn, kept for the next step
-          const double A_ = Gt[0 + c] - Gt[6 + c], B_ = Gt[3 + c] - Gt[9 + c];
-          const double C_ = Gt[0 + c] + Gt[6 + c], D_ = Gt[3 + c] + Gt[9 + c];
+        for (int c = 0; c < 3; ++c) {
+          const double m00 = GS[(0 + c) * NT + t] + Gb[0 + c];
+          const double m10 = GS[(3 + c) * NT + t] + Gb[3 + c];
+          const double m01 = GS[(6 + c) * NT + t] + Gb[6 + c];
+          const double m11 = GS[(9 + c) * NT + t] + Gb[9 + c];
+          const double A_ = m00 - m01, B_ = m10 - m11, C_ = m00 + m01, D_ = m10 + m11;
           const double y00 = A_ - B_, y10 = A_ + B_, y01 = C_ - D_, y11 = C_ + D_;
-          const double tup = y01 + __shfl_up_sync(0xffffffffu, y11, 1);
-          const double tdn = y00 + __shfl_up_sync(0xffffffffu, y10, 1);
-          if (it >= 2) {
-            const double A2 = Gb[0 + c] - Gb[6 + c], B2 = Gb[3 + c] - Gb[9 + c];
-            const double C2 = Gb[0 + c] + Gb[6 + c], D2 = Gb[3 + c] + Gb[9 + c];
-            const double b00 = A2 - B2, b10 = A2 + B2, b01 = C2 - D2, b11 = C2 + D2;
-            cup[c] = GS[c * NT + t] + (b01 + __shfl_up_sync(0xffffffffu, b11, 1));
-            CD[c * NT + t] = GS[(3 + c) * NT + t] + (b00 + __shfl_up_sync(0xffffffffu, b10, 1));
-          }
-          GS[c * NT + t] = tup;
-          GS[(3 + c) * NT + t] = tdn;
+          cup[c] = y01 + __shfl_up_sync(0xffffffffu, y11, 1);
+          CD[c * NT + t] = y00 + __shfl_up_sync(0xffffffffu, y10, 1);
         }
       }
+#pragma unroll
+      for (int i = 0; i < 12; ++i) GS[i * NT + t] = Gt[i];
     }
     __syncthreads();  // CD complete
     if (it >= 2 && mine) {
@@ -878,7 +871,7 @@ int op_tiles(const Grid& g) {
 }
 
 size_t op_smem(int /*mode*/) {
-  return sizeof(double) * ((size_t)NS * STAGE + 21 * NT + 168) + sizeof(uint64_t) * NS + 16;
+  return sizeof(double) * ((size_t)NS * STAGE + 27 * NT + 168) + sizeof(uint64_t) * NS + 16;
 }
 
 static void op_attr() {

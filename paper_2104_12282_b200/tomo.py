@@ -107,6 +107,8 @@ def load_library(path: str = LIB_PATH):
                                "paper_2104_12282_b200.build); there is no CPU fallback")
         lib = C.CDLL(path)
         for name, res, args in _SIGS:
+            if os.environ.get("TOMO_LIB_PATH") and not hasattr(lib, name):
+                continue  # A/B timing of an older build (scripts/build_variant.sh)
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
