@@ -230,8 +230,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         _, c, _, info = step()
     iters = info.iterations
-    # ---- timed region: inputs resident in HBM; per-launch K_A/K_B events (live profiling)
-    t.set_profiling(True)
+    # ---- timed region: inputs resident in HBM, no instrumentation
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
@@ -246,8 +245,6 @@ def run_ours(args):
     barrier()
     ck = clocks.stop()
     launches = t.launches - l0
-    prof = t.profile_times()
-    t.set_profiling(False)
     ms = e0.elapsed_time(e1)
     if world > 1:
         tt = torch.tensor([ms], device=dev)
@@ -255,6 +252,13 @@ def run_ours(args):
         ms = float(tt.item())
     ms_per_step = ms / args.steps
     value = world * args.steps / (ms * 1e-3)
+    # ---- one more, instrumented step: CUDA events around every PCG launch on the bound
+    # stream give the dominant kernel's per-launch device time for the roofline
+    t.set_profiling(True)
+    step()
+    barrier()
+    prof = t.profile_times()
+    t.set_profiling(False)
 
     # ---- e2e: through the C ABI with pinned host buffers (H2D rho, D2H P^T dc + c)
     e2e = None
@@ -286,7 +290,8 @@ def run_ours(args):
             "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
             "traffic": TRAFFIC.get(cfg), "peak_source": peak_src, "alg_bytes_per_launch": bytes_ka,
             "launch_ms": prof["k_a_ms"], "launches_timed": prof["n"],
-            "share_of_step": (prof["k_a_ms"] * (iters + 1)) / ms_per_step if ms_per_step else None}
+            "share_of_step": (prof["k_a_ms"] * (iters + 1)) / ms_per_step if ms_per_step else None,
+            "timing": "per-launch CUDA events over one instrumented evaluation after the timed region"}
     gf, _ = t.bench_dfma()
 
     cpu = None
