@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -49,6 +50,8 @@ struct tomo_ctx {
   int sms = 148;
   // operator launch variants (tensor maps bound to workspace buffers)
   OpArgs op_apply_u{}, op_apply_p0{}, op_pcg[2];  // op_pcg[k & 1] for launch k
+  cudaGraph_t pcg_graph = nullptr;        // WHILE(not done) { launch even; launch odd }
+  cudaGraphExec_t pcg_exec = nullptr;
   // profiling
   bool prof = false;
   double prof_a_ms = 0, prof_b_ms = 0;
@@ -403,6 +406,8 @@ extern "C" size_t tomo_workspace_bytes(const tomo_ctx* c) { return c ? c->off_en
 
 extern "C" void tomo_destroy(tomo_ctx* c) {
   if (!c) return;
+  if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
+  if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
   for (auto e : c->ev) cudaEventDestroy(e);
   delete c;
 }
@@ -476,6 +481,36 @@ int build_op_args(tomo_ctx* c) {
 }
 }  // namespace
 
+namespace {
+// The whole PCG loop as one graph: a conditional WHILE node whose body is the even and the
+// odd launch; the last block of a launch that sets `done` clears the condition. Launches
+// after convergence inside the body exit at their first instruction.
+int build_pcg_graph(tomo_ctx* c) {
+  if (c->pcg_exec) { cudaGraphExecDestroy(c->pcg_exec); c->pcg_exec = nullptr; }
+  if (c->pcg_graph) { cudaGraphDestroy(c->pcg_graph); c->pcg_graph = nullptr; }
+  if (std::getenv("TOMO_NO_GRAPH")) return TOMO_OK;  // batched host loop (A/B timing)
+  CK(c, cudaGraphCreate(&c->pcg_graph, 0));
+  cudaGraphConditionalHandle h;
+  CK(c, cudaGraphConditionalHandleCreate(&h, c->pcg_graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode;
+  CK(c, cudaGraphAddNode(&cnode, c->pcg_graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  OpArgs a0 = c->op_pcg[0], a1 = c->op_pcg[1];
+  a0.cond = h;
+  a1.cond = h;
+  cudaGraphNode_t n0, n1;
+  CK(c, add_pcg_node(body, &n0, nullptr, 0, a0, c->op_blocks));
+  CK(c, add_pcg_node(body, &n1, &n0, 1, a1, c->op_blocks));
+  CK(c, cudaGraphInstantiate(&c->pcg_exec, c->pcg_graph, 0));
+  return TOMO_OK;
+}
+}  // namespace
+
 extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   if (!c) return TOMO_EINVAL;
   if (!d_ws || (reinterpret_cast<uintptr_t>(d_ws) & 255)) return fail(c, TOMO_EINVAL, "workspace must be 256-B aligned");
@@ -515,6 +550,7 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   c->nb_oc = std::min(oc_max_blocks(), (int)std::max<long long>(1, (g.ne + 255) / 256));
   if ((size_t)c->nb_oc * 2 > c->n_part) c->nb_oc = (int)(c->n_part / 2);
   if (int rc = build_op_args(c)) return rc;
+  if (int rc = build_pcg_graph(c)) return rc;
   CK(c, cudaStreamSynchronize(c->st));
   c->bound = true;
   return TOMO_OK;
@@ -558,6 +594,13 @@ int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) 
   int k = 0;  // launches issued
   int batch = 8;
   const bool prof = c->prof;
+  if (!prof && c->pcg_exec) {
+    // the whole loop on the device: one graph launch, one read-back
+    CK(c, cudaGraphLaunch(c->pcg_exec, c->st));
+    CK(c, cudaMemcpyAsync(&hs, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
+    CK(c, cudaStreamSynchronize(c->st));
+    c->launches += 2 * ((hs.iters + 2) / 2);  // kernel nodes executed (pairs)
+  } else {
   if (prof) {
     while (c->ev.size() < 2 * 257) {
       cudaEvent_t e;
@@ -589,6 +632,7 @@ int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) 
     }
     if (hs.done) break;
     if (batch < 128) batch *= 2;
+  }
   }
   if (hs.done == 3) {
     return fail(c, hs.status ? hs.status : TOMO_EBREAKDOWN,

@@ -528,6 +528,7 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
         }
         s->cntA = 0;
         __threadfence();
+        if (a.cond && s->done) cudaGraphSetConditional(a.cond, 0u);  // end the graph's loop
       }
     }
   }
@@ -888,6 +889,19 @@ cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st) {
   if (mode == OP_PCG) k_op<OP_PCG><<<nblocks, dim3(TX, BY), op_smem(1), st>>>(a);
   else k_op<OP_APPLY><<<nblocks, dim3(TX, BY), op_smem(0), st>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t add_pcg_node(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode_t* deps,
+                         size_t ndeps, const OpArgs& a, int nblocks) {
+  op_attr();
+  cudaKernelNodeParams kp = {};
+  void* args[] = {const_cast<OpArgs*>(&a)};
+  kp.func = reinterpret_cast<void*>(k_op<OP_PCG>);
+  kp.gridDim = dim3(nblocks);
+  kp.blockDim = dim3(TX, BY);
+  kp.sharedMemBytes = (unsigned)op_smem(1);
+  kp.kernelParams = args;
+  return cudaGraphAddKernelNode(node, g, deps, ndeps, &kp);
 }
 
 int op_occupancy(int mode) {

@@ -102,6 +102,7 @@ struct OpArgs {
   double* partials;     // PCG: five per block
   Scal* s;              // PCG
   int ntiles;           // x-y tiles; the grid is persistent (1-D, balanced)
+  unsigned long long cond;  // PCG in a CUDA graph: WHILE-node handle cleared when done (0: none)
 };
 
 // launch helpers (kernels.cu). All enqueue on `st`; return the launch error.
@@ -109,6 +110,9 @@ int op_tiles(const Grid& g);
 size_t op_smem(int mode);
 int op_occupancy(int mode);
 cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st);
+// kernel node of one PCG launch (args copied into the node)
+cudaError_t add_pcg_node(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode_t* deps,
+                         size_t ndeps, const OpArgs& a, int nblocks);
 cudaError_t launch_simp(const Grid& g, const double* rho, double* E, double E0, double Emin,
                         double penal, Scal* s, cudaStream_t st);
 cudaError_t launch_jacobi(const Grid& g, const double* E, double ke_diag, double* dinv,
