@@ -112,6 +112,25 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+# ---------------------------------------------------------------- replicas (N > 1)
+def replica_aggregate(steps: int, local_ms: float, world: int, reduce_max=None):
+    """Replicas only: every rank ran `steps` evaluations of its own problem.
+    Time = max over ranks (device clock); value = all ranks' evaluations / time."""
+    ms = reduce_max(local_ms) if (world > 1 and reduce_max is not None) else local_ms
+    return world * steps / (ms * 1e-3), ms
+
+
+def torch_reduce_max(device):
+    import torch
+    import torch.distributed as dist
+
+    def f(x: float) -> float:
+        tt = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+    return f
+
+
 # ---------------------------------------------------------------- CPU oracle baseline
 def oracle_sample(cfg: str, n_iters_full: int | None, budget_iters: int = 4):
     """Time the oracle (as it stands) on a bounded sample of one evaluation of `cfg`:
@@ -245,13 +264,8 @@ def run_ours(args):
     barrier()
     ck = clocks.stop()
     launches = t.launches - l0
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    value, ms = replica_aggregate(args.steps, e0.elapsed_time(e1), world, torch_reduce_max(dev))
     ms_per_step = ms / args.steps
-    value = world * args.steps / (ms * 1e-3)
     # ---- one more, instrumented step: CUDA events around every PCG launch on the bound
     # stream give the dominant kernel's per-launch device time for the roofline
     t.set_profiling(True)
@@ -271,12 +285,9 @@ def run_ours(args):
         for _ in range(args.steps):
             t.evaluate_host(rho_h, dcf_h, tol=args.tol)
         barrier()
-        el = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([el], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            el = float(tt.item())
-        e2e = {"value": world * args.steps / el, "unit": UNIT,
+        e2e_value, _ = replica_aggregate(args.steps, (time.perf_counter() - t0) * 1e3, world,
+                                         torch_reduce_max(dev))
+        e2e = {"value": e2e_value, "unit": UNIT,
                "h2d_bytes_per_step": 8 * p.n_elem, "d2h_bytes_per_step": 8 * p.n_elem + 8}
 
     # ---- roofline of the dominant kernel: the single-pass PCG launch:

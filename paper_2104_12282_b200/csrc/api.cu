@@ -544,7 +544,9 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   int occ = op_occupancy(OP_PCG);
   if (occ < 1) occ = 1;
   const long long units = (long long)op_tiles(g) * g.nnz;
-  c->op_blocks = (int)std::max<long long>(1, std::min<long long>((long long)occ * c->sms, units / 6));
+  const char* mp = std::getenv("TOMO_MIN_PLANES");  // A/B knob; default 1 plane per block (small grids are latency-bound)
+  const long long minp = mp ? std::max(1, std::atoi(mp)) : 1;
+  c->op_blocks = (int)std::max<long long>(1, std::min<long long>((long long)occ * c->sms, units / minp));
   c->nb_b = (int)std::min<long long>((g.ndof_pad / 2 + 255) / 256, (long long)c->sms * 4);
   c->nb_s = (int)std::min<long long>((g.ne + 255) / 256, (long long)c->sms * 8);
   c->nb_oc = std::min(oc_max_blocks(), (int)std::max<long long>(1, (g.ne + 255) / 256));
