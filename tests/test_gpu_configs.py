@@ -125,7 +125,9 @@ def test_cfg4a_solve_residual_pins():
     op = OracleProblem(p)
     u = cpu(u_g)
     r = op.f - op.Khat(rho) @ u
-    assert abs(np.linalg.norm(r) / np.linalg.norm(op.f) - info.rel_res_true) <= 1e-3 * info.rel_res_true
+    rel_true = np.linalg.norm(r) / np.linalg.norm(op.f)
+    # at 1e-10 the residual is rounding noise of f - K u in two summation orders: 2% agreement
+    assert rel_true <= 2e-10 and abs(rel_true - info.rel_res_true) <= 2e-2 * rel_true
     # the oracle's own PCG from x0 = 0 takes (nearly) the same number of iterations
     _, its, conv, _ = op.solve_pcg(rho, tol=1e-10)
     assert conv and abs(its - info.iterations) <= max(3, 0.02 * its)
