@@ -72,6 +72,10 @@ def _gold(name):
 
 
 def test_cfg2_mbb_half_beam_against_tight_oracle():
+    """configs[2] against the oracle's tight (1e-12) solution (reading A14). The GPU solves
+    to 1e-10 as BJ states: compliance is quadratic in the energy error (App. A-6) and must
+    agree to 1e-9; u and dc to max(1e-8, 4 delta) with delta the solver-noise floor measured
+    as the GPU's own 1e-10 vs 1e-12 difference; at 1e-12 both sides agree to 1e-8."""
     meta, gold = _gold("cfg2")
     p = inputs.CFG2
     rho = inputs.density_for("cfg2")
@@ -80,13 +84,20 @@ def test_cfg2_mbb_half_beam_against_tight_oracle():
     assert info.converged == 1
     assert abs(info.iterations - meta["pcg_iters_1e-10"]) <= max(3, 0.02 * meta["pcg_iters_1e-10"])
     assert abs(c - meta["c"]) <= 1e-9 * abs(meta["c"])
-    # u and dc at 1e-10: bounded by the solver-noise floor (reading A14); at 1e-12 the bar is 1e-8
-    u12, info12 = t.solve(gpu(rho), tol=1e-12)
+    u12, info12 = t.solve(gpu(rho), tol=1e-12, max_iters=200000)
+    assert info12.converged == 1
     assert rel(cpu(u12), gold["u"]) <= 1e-8
     dc12 = cpu(t.sensitivity(gpu(rho), u12))
     assert rel(dc12, gold["dc"]) <= 1e-8
-    assert rel(cpu(dcf), gold["dcf"]) <= 1e-6
-    assert rel(cpu(u_g), gold["u"]) <= 1e-6
+    delta = rel(cpu(u_g), cpu(u12))
+    assert rel(cpu(u_g), gold["u"]) <= max(1e-8, 4 * delta), delta
+    dc = cpu(t.sensitivity(gpu(rho), u_g))
+    bar_dc = max(1e-8, 4 * rel(dc, dc12))
+    assert rel(dc, gold["dc"]) <= bar_dc
+    assert rel(cpu(dcf), gold["dcf"]) <= bar_dc
+    # operator-level parity on the oracle's own u (no solver noise)
+    dc_on_gold = cpu(t.sensitivity(gpu(rho), gpu(gold["u"])))
+    assert rel(dc_on_gold, gold["dc"]) <= 1e-12
 
 
 def test_cfg0_against_stored_tight_oracle_if_present():
