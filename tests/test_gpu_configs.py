@@ -128,6 +128,10 @@ def test_cfg4_operator_parity(idx, variant):
 
 
 def test_cfg4a_solve_residual_pins():
+    """32^3 with 70% of the elements at E = Emin = 1e-9 (configs[4] void 0.7). At this
+    contrast CG loses orthogonality and its iteration count depends on rounding (measured:
+    GPU 11,211 vs the oracle's textbook PCG 15,310, both converged), so the pin is the true
+    residual of u_gpu under the oracle's own K_hat, not the count."""
     p = inputs.cfg4(0)
     rho = inputs.density_void07(p)
     t = ctx(p)
@@ -139,9 +143,7 @@ def test_cfg4a_solve_residual_pins():
     rel_true = np.linalg.norm(r) / np.linalg.norm(op.f)
     # at 1e-10 the residual is rounding noise of f - K u in two summation orders: 2% agreement
     assert rel_true <= 2e-10 and abs(rel_true - info.rel_res_true) <= 2e-2 * rel_true
-    # the oracle's own PCG from x0 = 0 takes (nearly) the same number of iterations
-    _, its, conv, _ = op.solve_pcg(rho, tol=1e-10)
-    assert conv and abs(its - info.iterations) <= max(3, 0.02 * its)
+    assert abs(info.rel_res_recursive) <= 1e-10
 
 
 # ------------------------------------------------------------------ configs[1]: 50-step loop
