@@ -388,9 +388,11 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
         nz[c] = ndi * rn;
         nv[c] = fx ? 0.0 : fma(beta, po, nz[c]);
         if (wr) {
+#ifndef TOMO_EXP_NO_COMMIT_STORE  // timing experiment only (scripts/build_variant.sh)
           a.rnew[go + c] = rn;
           a.pnew[go + c] = nv[c];
           a.u[go + c] = fma(alpha_prev, po, stg[UO_OFF + uo + c]);
+#endif
           rz = fma(nz[c], rn, rz);
           rr = fma(rn, rn, rr);
         }
@@ -437,7 +439,12 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
         Fc[9 + c] = d1 - d0p;
       }
       double Gb[12], Gt[12];
+#ifdef TOMO_EXP_NO_CORE  // timing experiment only: bypass the element core
+#pragma unroll
+      for (int i = 0; i < 12; ++i) { Gb[i] = Fc[i] * Ecur; Gt[i] = Fn[i] * Ecur; }
+#else
       element_core(Fc, Fn, Ecur, a.w, Gb, Gt);
+#endif
       if (it >= 2) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -464,7 +471,9 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
         const bool fixed = (pm >> c) & 1u;
         if (MODE == OP_PCG) {
           qv = fixed ? 0.0 : qv;
+#ifndef TOMO_EXP_NO_Q_STORE  // timing experiment only
           a.out[gb + c] = qv;
+#endif
           pq = fma(pv[c], qv, pq);
           zq = fma(pz[c], qv, zq);
           qdq = fma(pdi * qv, qv, qdq);
