@@ -512,7 +512,12 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
         s->pq = pq;
         s->rz = rz;
         s->rr = rr;
+#ifdef TOMO_EXP_NOSTOP  // timing experiments: run exactly max_iters launches whatever the values
+        if (k >= s->max_iters) { s->done = 2; s->iters = k; } else { s->alpha = 0.5; s->beta = 0.5; s->k = k + 1; }
+        if (false) {
+#else
         if (!isfinite(pq) || !isfinite(rz) || !isfinite(rr) || !isfinite(zq) || !isfinite(qdq)) {
+#endif
           s->status = -6;  // TOMO_ENAN
           s->done = 3;
           s->iters = k;
