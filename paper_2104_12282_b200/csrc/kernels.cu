@@ -355,7 +355,10 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
   const int gi = i0 - 1 + tx, gj = j0 - 1 + ty;
   const bool mine = tx >= 1 && tx <= OX && ty >= 1 && ty <= OY && gi <= g.nx && gj <= g.ny;
   const int g_node = 3 * gi + rowd * gj;                 // + planed * plane
-  const int uo = (ty - 1) * OWN_W + 3 * (tx - 1);
+  // owned row segment of this warp: nodes i0..i0+29 of node row gj (rows 1..OY of the tile)
+  const bool own_row = ty >= 1 && ty <= OY && gj <= g.ny;
+  const int g_row = 3 * i0 + rowd * gj;                  // + planed * plane
+  const int own_lim = 3 * min(OX, g.nx - i0 + 1);        // doubles of the segment in the domain
   const int fv = ty * VB_W + org.ov + 3 * tx;
   const int fd = ty * DB_W + org.od + tx;
   const int fm = ty * MB_W + org.om + tx;
@@ -373,32 +376,46 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
     mbar_wait(&bars[s], (unsigned)(git / NS) & 1u);
     const int kn = kbeg - 1 + it;  // node plane of this step
     // ---- commit my node: p = D^-1 r + beta p_old, r = r_old - alpha q_old (PCG)
-    const unsigned m = reinterpret_cast<const unsigned char*>(stg + MK_OFF)[fm];
+    const unsigned char* MKb = reinterpret_cast<const unsigned char*>(stg + MK_OFF);
+    const unsigned m = MKb[fm];
     double nv[3], nz[3], ndi = 0.0;
     if (MODE == OP_PCG) {
-      const bool wr = mine && kn >= kbeg && kn < kend;
       ndi = stg[DI_OFF + fd];
-      const int go = g_node + planed * kn;
-      double rz = 0.0, rr = 0.0;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const bool fx = (m >> c) & 1u;
-        const double po = stg[PO_OFF + fv + c];
         const double rn = fx ? 0.0 : fma(-alpha_prev, stg[QO_OFF + fv + c], stg[R_OFF + fv + c]);
         nz[c] = ndi * rn;
-        nv[c] = fx ? 0.0 : fma(beta, po, nz[c]);
-        if (wr) {
-#ifndef TOMO_EXP_NO_COMMIT_STORE  // timing experiment only (scripts/build_variant.sh)
-          a.rnew[go + c] = rn;
-          a.pnew[go + c] = nv[c];
-          a.u[go + c] = fma(alpha_prev, po, stg[UO_OFF + uo + c]);
-#endif
-          rz = fma(nz[c], rn, rz);
-          rr = fma(rn, rn, rr);
-        }
+        nv[c] = fx ? 0.0 : fma(beta, stg[PO_OFF + fv + c], nz[c]);
       }
-      acc[1] += rz;
-      acc[2] += rr;
+      // owned updates, coalesced: lane l handles doubles l, l+32, l+64 of this warp's
+      // 90-double owned row segment (nodes i0..i0+29), recomputing r, p from the stage
+      if (own_row && kn >= kbeg && kn < kend) {
+        const int grow = g_row + planed * kn;
+        double rz = 0.0, rr = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int pos = tx + 32 * q;  // position in the owned segment
+          if (pos < own_lim) {
+            const int nd = pos / 3, c = pos - 3 * nd;  // node 1 + nd of the tile row, comp c
+            const int f = ty * VB_W + org.ov + 3 + pos;
+            const bool fx = (MKb[ty * MB_W + org.om + 1 + nd] >> c) & 1u;
+            const double di = stg[DI_OFF + ty * DB_W + org.od + 1 + nd];
+            const double po = stg[PO_OFF + f];
+            const double rn = fx ? 0.0 : fma(-alpha_prev, stg[QO_OFF + f], stg[R_OFF + f]);
+            const double z = di * rn;
+#ifndef TOMO_EXP_NO_COMMIT_STORE  // timing experiment only (scripts/build_variant.sh)
+            a.rnew[grow + pos] = rn;
+            a.pnew[grow + pos] = fx ? 0.0 : fma(beta, po, z);
+            a.u[grow + pos] = fma(alpha_prev, po, stg[UO_OFF + (ty - 1) * OWN_W + pos]);
+#endif
+            rz = fma(z, rn, rz);
+            rr = fma(rn, rn, rr);
+          }
+        }
+        acc[1] += rz;
+        acc[2] += rr;
+      }
     } else {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
