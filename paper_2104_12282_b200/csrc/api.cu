@@ -432,7 +432,7 @@ int build_op_args(tomo_ctx* c) {
   const uint64_t rowm = (uint64_t)g.mp, planem = rowm * g.nny;
   const uint64_t rowe = 8ull * g.nx_pad, planee = rowe * g.ny;
   const CUtensorMapDataType F64 = CU_TENSOR_MAP_DATA_TYPE_FLOAT64, U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
-  const uint32_t inw = 3 * (OP_OX + 2) + 2, inh = OP_BY;  // boxes widened: aligned starts
+  const uint32_t inw = 3 * (OP_OX + 2) + 2, inh = OP_BY + 1;  // boxes widened: aligned starts
   CUtensorMap tm_u, tm_uown, tm_r[2], tm_q[2], tm_p[2], tm_dinv, tm_mask, tm_E;
   int rc;
   auto vec = [&](CUtensorMap* tm, double* base, uint32_t b0, uint32_t b1) {
@@ -447,7 +447,7 @@ int build_op_args(tomo_ctx* c) {
   }
   if ((rc = make_map(c, &tm_dinv, F64, c->dinv(), g.nnx, g.nny, g.nnz, rown, planen, OP_OX + 4, inh))) return rc;
   if ((rc = make_map(c, &tm_mask, U8, c->dmask(), g.nnx, g.nny, g.nnz, rowm, planem, 48, inh))) return rc;
-  if ((rc = make_map(c, &tm_E, F64, c->E(), g.nx, g.ny, g.nz, rowe, planee, 32, OP_BY - 1))) return rc;
+  if ((rc = make_map(c, &tm_E, F64, c->E(), g.nx, g.ny, g.nz, rowe, planee, 32, OP_BY))) return rc;
   OpArgs base{};
   base.tm_uown = tm_uown;
   base.tm_dinv = tm_dinv;

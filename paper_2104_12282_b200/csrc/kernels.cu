@@ -35,8 +35,8 @@ constexpr int NT = TX * BY;            // threads per operator block
 constexpr int OX = OP_OX;              // output nodes per tile along x
 constexpr int OY = OP_OY;              // output nodes per tile along y
 constexpr int NS = OP_NS;              // pipeline stages
-constexpr int NR = BY;                 // node rows per tile (one per warp)
-constexpr int ER = BY - 1;             // element rows per tile
+constexpr int NR = BY + 1;             // node rows per tile (warp w stages rows w, w+1)
+constexpr int ER = BY;                 // element rows per tile (one per warp)
 constexpr int OWN_W = 3 * OX;          // 90 doubles per owned row
 constexpr int OWN_N = OWN_W * OY;      // 540
 // TMA boxes. The innermost box start must be 16-byte aligned (measured on this B200: an
@@ -302,9 +302,8 @@ template <int MODE>
 __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpArgs a) {
   extern __shared__ __align__(128) double smem[];
   double* stages = smem;                     // [NS][STAGE]
-  double* XE = stages + NS * STAGE;          // [2][6][NT] x-edge sums / differences (by plane parity)
-  double* CD = XE + 12 * NT;                 // [3][NT] row-ty contributions to row ty-1
-  double* GS = CD + 3 * NT;                  // [12][NT] thread-private: top-face sums of the last element
+  double* CD = stages + NS * STAGE;          // [2][3][NT] bottom-face contributions (by parity)
+  double* GS = CD + 6 * NT;                  // [12][NT] thread-private: top-face sums of the last element
   double* red = GS + 12 * NT;                // [168]
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 168);  // [NS]
   int* s_flag = reinterpret_cast<int*>(bars + NS);
@@ -351,45 +350,50 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
                         kbeg - 1 + s);
   }
 
-  // my node (i0-1+tx, j0-1+ty); it is an output ("mine") inside the owned 30 x 6 block
-  const int gi = i0 - 1 + tx, gj = j0 - 1 + ty;
-  const bool mine = tx >= 1 && tx <= OX && ty >= 1 && ty <= OY && gi <= g.nx && gj <= g.ny;
-  const int g_node = 3 * gi + rowd * gj;                 // + planed * plane
-  // owned row segment of this warp: nodes i0..i0+29 of node row gj (rows 1..OY of the tile)
-  const bool own_row = ty >= 1 && ty <= OY && gj <= g.ny;
-  const int g_row = 3 * i0 + rowd * gj;                  // + planed * plane
+  // output node (i0-1+tx, j0+ty) = top node of this warp's element row
+  const int gi = i0 - 1 + tx, gj = j0 + ty;
+  const bool own_row = ty < OY && gj <= g.ny;
+  const bool mine = own_row && tx >= 1 && tx <= OX && gi <= g.nx;
+  const int g_row = 3 * i0 + rowd * gj;                  // owned segment, + planed * plane
   const int own_lim = 3 * min(OX, g.nx - i0 + 1);        // doubles of the segment in the domain
-  const int fv = ty * VB_W + org.ov + 3 * tx;
-  const int fd = ty * DB_W + org.od + tx;
-  const int fm = ty * MB_W + org.om + tx;
-  const int fe = (ty - 1) * E_W + org.oe + tx;          // element (tx, ty), ty >= 1
+  const int fvb = ty * VB_W + org.ov + 3 * tx;           // node rows ty (b) and ty+1 (o) in the
+  const int fvo = fvb + VB_W;                            // vector box
+  const int fdb = ty * DB_W + org.od + tx, fdo = fdb + DB_W;
+  const int fmb = ty * MB_W + org.om + tx, fmo = fmb + MB_W;
+  const int fe = ty * E_W + org.oe + tx;                 // element (tx, ty)
 
-  // my node in the previous plane: p and z (PCG) or raw u (APPLY), D^-1, fixed bits
+  // previous plane: node values of rows b, o (for the lower face) and the output node's
+  // p, z (PCG) or raw u (APPLY), D^-1, fixed bits
+  double vb_p[3] = {0.0, 0.0, 0.0}, vo_p[3] = {0.0, 0.0, 0.0};
   double pv[3] = {0.0, 0.0, 0.0}, pz[3] = {0.0, 0.0, 0.0}, pdi = 0.0;
   unsigned pm = 0;
 
   for (int it = 0; it < nit; ++it, ++git) {
     const int s = git % NS;
     double* stg = stages + s * STAGE;
-    double* XEn = XE + (it & 1) * 6 * NT;        // this plane's x-edges
-    double* XEp = XE + ((it & 1) ^ 1) * 6 * NT;  // previous plane's x-edges
+    double* CDn = CD + (it & 1) * 3 * NT;
     mbar_wait(&bars[s], (unsigned)(git / NS) & 1u);
     const int kn = kbeg - 1 + it;  // node plane of this step
-    // ---- commit my node: p = D^-1 r + beta p_old, r = r_old - alpha q_old (PCG)
+    // ---- stage node rows b = ty and o = ty+1: p = D^-1 r + beta p_old with
+    //      r = r_old - alpha q_old (PCG), or masked u (APPLY)
     const unsigned char* MKb = reinterpret_cast<const unsigned char*>(stg + MK_OFF);
-    const unsigned m = MKb[fm];
-    double nv[3], nz[3], ndi = 0.0;
+    const unsigned mb = MKb[fmb], mo = MKb[fmo];
+    double vb[3], vo[3], zo[3], dio = 0.0;
     if (MODE == OP_PCG) {
-      ndi = stg[DI_OFF + fd];
+      const double dib = stg[DI_OFF + fdb];
+      dio = stg[DI_OFF + fdo];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const bool fx = (m >> c) & 1u;
-        const double rn = fx ? 0.0 : fma(-alpha_prev, stg[QO_OFF + fv + c], stg[R_OFF + fv + c]);
-        nz[c] = ndi * rn;
-        nv[c] = fx ? 0.0 : fma(beta, stg[PO_OFF + fv + c], nz[c]);
+        const double rb = ((mb >> c) & 1u) ? 0.0
+                          : fma(-alpha_prev, stg[QO_OFF + fvb + c], stg[R_OFF + fvb + c]);
+        vb[c] = ((mb >> c) & 1u) ? 0.0 : fma(beta, stg[PO_OFF + fvb + c], dib * rb);
+        const double ro = ((mo >> c) & 1u) ? 0.0
+                          : fma(-alpha_prev, stg[QO_OFF + fvo + c], stg[R_OFF + fvo + c]);
+        zo[c] = dio * ro;
+        vo[c] = ((mo >> c) & 1u) ? 0.0 : fma(beta, stg[PO_OFF + fvo + c], zo[c]);
       }
-      // owned updates, coalesced: lane l handles doubles l, l+32, l+64 of this warp's
-      // 90-double owned row segment (nodes i0..i0+29), recomputing r, p from the stage
+      // owned updates of node row o, coalesced: lane l handles doubles l, l+32, l+64 of the
+      // 90-double owned segment (nodes i0..i0+29), recomputed from the stage
       if (own_row && kn >= kbeg && kn < kend) {
         const int grow = g_row + planed * kn;
         double rz = 0.0, rr = 0.0;
@@ -398,16 +402,16 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
           const int pos = tx + 32 * q;  // position in the owned segment
           if (pos < own_lim) {
             const int nd = pos / 3, c = pos - 3 * nd;  // node 1 + nd of the tile row, comp c
-            const int f = ty * VB_W + org.ov + 3 + pos;
-            const bool fx = (MKb[ty * MB_W + org.om + 1 + nd] >> c) & 1u;
-            const double di = stg[DI_OFF + ty * DB_W + org.od + 1 + nd];
+            const int f = (ty + 1) * VB_W + org.ov + 3 + pos;
+            const bool fx = (MKb[(ty + 1) * MB_W + org.om + 1 + nd] >> c) & 1u;
+            const double di = stg[DI_OFF + (ty + 1) * DB_W + org.od + 1 + nd];
             const double po = stg[PO_OFF + f];
             const double rn = fx ? 0.0 : fma(-alpha_prev, stg[QO_OFF + f], stg[R_OFF + f]);
             const double z = di * rn;
 #ifndef TOMO_EXP_NO_COMMIT_STORE  // timing experiment only (scripts/build_variant.sh)
             a.rnew[grow + pos] = rn;
             a.pnew[grow + pos] = fx ? 0.0 : fma(beta, po, z);
-            a.u[grow + pos] = fma(alpha_prev, po, stg[UO_OFF + (ty - 1) * OWN_W + pos]);
+            a.u[grow + pos] = fma(alpha_prev, po, stg[UO_OFF + ty * OWN_W + pos]);
 #endif
             rz = fma(z, rn, rz);
             rr = fma(rn, rn, rr);
@@ -419,41 +423,25 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
     } else {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        nz[c] = stg[R_OFF + fv + c];  // raw u (identity rows at fixed DOFs)
-        nv[c] = ((m >> c) & 1u) ? 0.0 : nz[c];
+        vb[c] = ((mb >> c) & 1u) ? 0.0 : stg[R_OFF + fvb + c];
+        zo[c] = stg[R_OFF + fvo + c];  // raw u (identity rows at fixed DOFs)
+        vo[c] = ((mo >> c) & 1u) ? 0.0 : zo[c];
       }
     }
-    const double Ecur = (ty >= 1) ? stg[EE_OFF + fe] : 0.0;  // lane 31: unused column
-    // ---- x-edges of my node row (partner: lane + 1)
-    double xs[3], xd[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double an = __shfl_down_sync(0xffffffffu, nv[c], 1);
-      xs[c] = nv[c] + an;
-      xd[c] = an - nv[c];
-      XEn[c * NT + t] = xs[c];
-      XEn[(3 + c) * NT + t] = xd[c];
-    }
-    __syncthreads();  // XE complete; stage s consumed
-    if (t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
-    // (a segment's last NS steps issue nothing, so the next segment starts with free stages)
+    const double Ecur = stg[EE_OFF + fe];  // lane 31: a column outside the tile (unused)
 
+    // ---- element row ty between node rows b and o (lane 31's results are never read)
     double cup[3] = {0.0, 0.0, 0.0};
-    if (ty >= 1 && it >= 1) {  // warp-uniform: element row ty between node rows ty-1 and ty
+    if (it >= 1) {
       double Fc[12], Fn[12];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double s0 = XEn[c * NT + t - TX], d0 = XEn[(3 + c) * NT + t - TX];
-        Fn[0 + c] = s0 + xs[c];
-        Fn[3 + c] = d0 + xd[c];
-        Fn[6 + c] = xs[c] - s0;
-        Fn[9 + c] = xd[c] - d0;
-        const double s1 = XEp[c * NT + t], d1 = XEp[(3 + c) * NT + t];
-        const double s0p = XEp[c * NT + t - TX], d0p = XEp[(3 + c) * NT + t - TX];
-        Fc[0 + c] = s0p + s1;
-        Fc[3 + c] = d0p + d1;
-        Fc[6 + c] = s1 - s0p;
-        Fc[9 + c] = d1 - d0p;
+        const double bn = __shfl_down_sync(0xffffffffu, vb[c], 1);
+        const double on = __shfl_down_sync(0xffffffffu, vo[c], 1);
+        const double bnp = __shfl_down_sync(0xffffffffu, vb_p[c], 1);
+        const double onp = __shfl_down_sync(0xffffffffu, vo_p[c], 1);
+        face_from(vb[c], bn, vo[c], on, Fn, c);
+        face_from(vb_p[c], bnp, vo_p[c], onp, Fc, c);
       }
       double Gb[12], Gt[12];
 #ifdef TOMO_EXP_NO_CORE  // timing experiment only: bypass the element core
@@ -471,20 +459,23 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
           const double m11 = GS[(9 + c) * NT + t] + Gb[9 + c];
           const double A_ = m00 - m01, B_ = m10 - m11, C_ = m00 + m01, D_ = m10 + m11;
           const double y00 = A_ - B_, y10 = A_ + B_, y01 = C_ - D_, y11 = C_ + D_;
-          cup[c] = y01 + __shfl_up_sync(0xffffffffu, y11, 1);
-          CD[c * NT + t] = y00 + __shfl_up_sync(0xffffffffu, y10, 1);
+          cup[c] = y01 + __shfl_up_sync(0xffffffffu, y11, 1);   // -> node row o (mine)
+          CDn[c * NT + t] = y00 + __shfl_up_sync(0xffffffffu, y10, 1);  // -> node row b
         }
       }
 #pragma unroll
       for (int i = 0; i < 12; ++i) GS[i * NT + t] = Gt[i];
     }
-    __syncthreads();  // CD complete
+    __syncthreads();  // CD of this plane complete; stage s consumed by every warp
+    if (t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
+    // (a segment's last NS steps issue nothing, so the next segment starts with free stages)
+
     if (it >= 2 && mine) {
-      const int gb = g_node + planed * (kn - 1);  // output node plane kn - 1
+      const int gb = 3 * gi + rowd * gj + planed * (kn - 1);  // output node plane kn - 1
       double pq = 0.0, zq = 0.0, qdq = 0.0;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        double qv = cup[c] + CD[c * NT + t + TX];
+        double qv = cup[c] + CDn[c * NT + t + TX];  // + bottom face of element row ty+1
         const bool fixed = (pm >> c) & 1u;
         if (MODE == OP_PCG) {
           qv = fixed ? 0.0 : qv;
@@ -503,11 +494,16 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
       acc[4] += qdq;
     }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { pv[c] = nv[c]; pz[c] = nz[c]; }
-    pdi = ndi;
-    pm = m;
+    for (int c = 0; c < 3; ++c) {
+      vb_p[c] = vb[c];
+      vo_p[c] = vo[c];
+      pv[c] = vo[c];
+      pz[c] = zo[c];
+    }
+    pdi = dio;
+    pm = mo;
   }
-  __syncthreads();  // segment done: XE / GS / stages may be reused by the next segment
+  __syncthreads();  // segment done: CD / GS / stages may be reused by the next segment
   }
 
   if (MODE == OP_PCG) {
@@ -903,7 +899,7 @@ int op_tiles(const Grid& g) {
 }
 
 size_t op_smem(int /*mode*/) {
-  return sizeof(double) * ((size_t)NS * STAGE + 27 * NT + 168) + sizeof(uint64_t) * NS + 16;
+  return sizeof(double) * ((size_t)NS * STAGE + 18 * NT + 168) + sizeof(uint64_t) * NS + 16;
 }
 
 static void op_attr() {

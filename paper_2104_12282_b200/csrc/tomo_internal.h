@@ -71,10 +71,12 @@ struct Scal {
 
 enum OpMode { OP_APPLY = 0, OP_PCG = 1 };
 
-// Operator tile: 32 x OP_BY threads. Warp ty stages node row j0-1+ty (OP_BY node rows);
-// thread (tx, ty >= 1) computes element column (i0-1+tx, j0-2+ty) (OP_BY-1 element rows);
-// thread (tx, ty) outputs node (i0-1+tx, j0-1+ty) for 1 <= tx <= OP_OX, 1 <= ty <= OP_OY.
-// x-neighbours are exchanged with warp shuffles, y-neighbours through shared memory.
+// Operator tile: 32 x OP_BY threads. Warp w stages node rows w and w+1 of the tile (OP_BY+1
+// node rows j0-1 .. j0+OP_BY-1, the shared row staged by both warps), computes element row
+// w (element column i0-1+tx in lane tx; lane 31 is outside the tile) and outputs node row
+// w+1 (OP_OY = OP_BY-1 output rows j0 .. j0+OP_BY-2, OP_OX = 30 output columns i0 .. i0+29).
+// x-neighbours are exchanged with warp shuffles; the only cross-warp exchange is the
+// bottom-face contribution of element row w+1 to node row w+1 (one barrier per plane).
 // A block marches along z through a chunk of node planes.
 #ifndef TOMO_OP_BY
 #define TOMO_OP_BY 8
@@ -82,7 +84,7 @@ enum OpMode { OP_APPLY = 0, OP_PCG = 1 };
 constexpr int OP_BY = TOMO_OP_BY;
 constexpr int OP_MINB = OP_BY >= 16 ? 1 : 2;  // resident blocks per SM the tile is sized for
 constexpr int OP_OX = 30;           // output nodes per tile along x (even: 16-B TMA rows)
-constexpr int OP_OY = OP_BY - 2;    // output nodes per tile along y
+constexpr int OP_OY = OP_BY - 1;    // output nodes per tile along y
 constexpr int OP_NS = 2;            // TMA pipeline stages (node planes in flight)
 
 struct OpArgs {
