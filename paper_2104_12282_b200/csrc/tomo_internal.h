@@ -86,6 +86,13 @@ constexpr int OP_MINB = OP_BY >= 16 ? 1 : 2;  // resident blocks per SM the tile
 constexpr int OP_OX = 30;           // output nodes per tile along x (even: 16-B TMA rows)
 constexpr int OP_OY = OP_BY - 1;    // output nodes per tile along y
 constexpr int OP_NS = 2;            // TMA pipeline stages (node planes in flight)
+#ifndef TOMO_OP_PF
+#define TOMO_OP_PF 0
+#endif
+// L2 prefetch distance (planes beyond the staged one); 0 = off. Measured at cfg3: off 79.8 us,
+// 2: 82.5, 3: 88.1, 4: 97.8, 6: 106.5 us per launch — extra TMA requests cost more than the
+// latency they hide, so it stays off.
+constexpr int OP_PF = TOMO_OP_PF;
 
 struct OpArgs {
   CUtensorMap tm_in;    // APPLY: u ; PCG: r_{k-1} (box 98 x (BY+1) doubles)
