@@ -211,7 +211,7 @@ def run_reference(args):
 REF_ITERS = {"cfg3": 10488}
 # DRAM bytes per launch of the dominant kernel from one `ncu --set full` capture
 # (dram__bytes_read.sum + dram__bytes_write.sum), see profiles/.
-TRAFFIC: dict = {}
+TRAFFIC = {"cfg3": 334932992}  # r1: 226.8 MB read + 108.1 MB written (profiles/r1_pcg_kernel_ncu.json)
 
 
 # ---------------------------------------------------------------- our arm
