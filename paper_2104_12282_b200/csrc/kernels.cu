@@ -46,17 +46,30 @@ constexpr int VB_W = 3 * (OX + 2) + 2; // 98 doubles: vector rows (start offset 
 constexpr int DB_W = OX + 4;           // 34 doubles: Jacobi rows (start offset 0..1)
 constexpr int MB_W = 48;               // 48 bytes: mask rows (start offset 0..15)
 constexpr int E_W = 32;                // element box width (start offset 0..1, 31 used)
+#ifdef TOMO_GS6
+constexpr int GSN = 6;                 // top face carried as node sums
+#else
+constexpr int GSN = 12;                // top face carried as Walsh face modes
+#endif
 // stage layout in doubles, every piece 128-byte aligned
 constexpr int al16(int n) { return (n + 15) & ~15; }  // doubles -> multiple of 128 B
 constexpr int R_OFF = 0;                                       // r_{k-1} (APPLY: u)
 constexpr int QO_OFF = R_OFF + al16(VB_W * NR);                // q_{k-1}
 constexpr int PO_OFF = QO_OFF + al16(VB_W * NR);               // p_{k-1}
 constexpr int UO_OFF = PO_OFF + al16(VB_W * NR);               // u, owned box
+#ifdef TOMO_U_LDG
+constexpr int DI_OFF = UO_OFF;                                 // D^-1 (u is not staged)
+#else
 constexpr int DI_OFF = UO_OFF + al16(OWN_N);                   // D^-1
+#endif
 constexpr int EE_OFF = DI_OFF + al16(DB_W * NR);               // E
 constexpr int MK_OFF = EE_OFF + al16(E_W * ER);                // mask bytes
 constexpr int STAGE = MK_OFF + al16((MB_W * NR + 7) / 8);
+#ifdef TOMO_U_LDG
+constexpr unsigned BYTES_PCG = 8u * (3 * VB_W * NR + DB_W * NR + E_W * ER) + MB_W * NR;
+#else
 constexpr unsigned BYTES_PCG = 8u * (3 * VB_W * NR + OWN_N + DB_W * NR + E_W * ER) + MB_W * NR;
+#endif
 constexpr unsigned BYTES_APPLY = 8u * (VB_W * NR + E_W * ER) + MB_W * NR;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -299,7 +312,9 @@ __device__ __forceinline__ void issue_plane(const OpArgs& a, double* stg, uint64
   if (MODE == OP_PCG) {
     tma_load_3d(stg + QO_OFF, &a.tm_qold, o.xv, j0 - 1, kq, bar);
     tma_load_3d(stg + PO_OFF, &a.tm_pold, o.xv, j0 - 1, kq, bar);
+#ifndef TOMO_U_LDG
     tma_load_3d(stg + UO_OFF, &a.tm_uown, 3 * i0, j0, kq, bar);
+#endif
     tma_load_3d(stg + DI_OFF, &a.tm_dinv, o.xd, j0 - 1, kq, bar);
   }
   tma_load_3d(stg + MK_OFF, &a.tm_mask, o.xm, j0 - 1, kq, bar);
@@ -324,8 +339,8 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
   extern __shared__ __align__(128) double smem[];
   double* stages = smem;                     // [NS][STAGE]
   double* CD = stages + NS * STAGE;          // [2][3][NT] bottom-face contributions (by parity)
-  double* GS = CD + 6 * NT;                  // [12][NT] thread-private: top-face sums of the last element
-  double* red = GS + 12 * NT;                // [168]
+  double* GS = CD + 6 * NT;                  // [GSN][NT] thread-private: top face of the last element
+  double* red = GS + GSN * NT;               // [168]
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 168);  // [NS]
   int* s_flag = reinterpret_cast<int*>(bars + NS);
 
@@ -393,8 +408,18 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
     const int s = git % NS;
     double* stg = stages + s * STAGE;
     double* CDn = CD + (it & 1) * 3 * NT;
-    mbar_wait(&bars[s], (unsigned)(git / NS) & 1u);
     const int kn = kbeg - 1 + it;  // node plane of this step
+#ifdef TOMO_U_LDG
+    // owned u of this plane: coalesced loads issued before the stage wait
+    double u_pre[3] = {0.0, 0.0, 0.0};
+    if (MODE == OP_PCG && own_row && kn >= kbeg && kn < kend) {
+      const int grow = g_row + planed * kn;
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (tx + 32 * q < own_lim) u_pre[q] = a.u[grow + tx + 32 * q];
+    }
+#endif
+    mbar_wait(&bars[s], (unsigned)(git / NS) & 1u);
 #ifdef TOMO_EXP_ONLY_LOAD  // timing experiment only: the TMA pipeline alone
     acc[0] += stg[R_OFF + t] + stg[QO_OFF + t] + stg[PO_OFF + t] + stg[UO_OFF + t];
     __syncthreads();
@@ -438,7 +463,11 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
 #ifndef TOMO_EXP_NO_COMMIT_STORE  // timing experiment only (scripts/build_variant.sh)
             a.rnew[grow + pos] = rn;
             a.pnew[grow + pos] = fx ? 0.0 : fma(beta, po, z);
+#ifdef TOMO_U_LDG
+            a.u[grow + pos] = fma(alpha_prev, po, u_pre[q]);
+#else
             a.u[grow + pos] = fma(alpha_prev, po, stg[UO_OFF + ty * OWN_W + pos]);
+#endif
 #endif
             rz = fma(z, rn, rz);
             rr = fma(rn, rn, rr);
@@ -477,6 +506,26 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
 #else
       element_core(Fc, Fn, Ecur, a.w, Gb, Gt);
 #endif
+#ifdef TOMO_GS6
+      // xy-inverse of each face separately, combined along x through the warp; the top face
+      // is carried to the next plane as 6 node sums (cup / cdn of node rows o / b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double A_ = Gt[0 + c] - Gt[6 + c], B_ = Gt[3 + c] - Gt[9 + c];
+        const double C_ = Gt[0 + c] + Gt[6 + c], D_ = Gt[3 + c] + Gt[9 + c];
+        const double tup = (C_ - D_) + __shfl_up_sync(0xffffffffu, C_ + D_, 1);
+        const double tdn = (A_ - B_) + __shfl_up_sync(0xffffffffu, A_ + B_, 1);
+        if (it >= 2) {
+          const double A2 = Gb[0 + c] - Gb[6 + c], B2 = Gb[3 + c] - Gb[9 + c];
+          const double C2 = Gb[0 + c] + Gb[6 + c], D2 = Gb[3 + c] + Gb[9 + c];
+          cup[c] = GS[c * NT + t] + ((C2 - D2) + __shfl_up_sync(0xffffffffu, C2 + D2, 1));
+          CDn[c * NT + t] = GS[(3 + c) * NT + t] + ((A2 - B2) + __shfl_up_sync(0xffffffffu, A2 + B2, 1));
+        }
+        GS[c * NT + t] = tup;
+        GS[(3 + c) * NT + t] = tdn;
+      }
+    }
+#else
       if (it >= 2) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -493,6 +542,7 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
 #pragma unroll
       for (int i = 0; i < 12; ++i) GS[i * NT + t] = Gt[i];
     }
+#endif
     __syncthreads();  // CD of this plane complete; stage s consumed by every warp
     if (t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
     // (a segment's last NS steps issue nothing, so the next segment starts with free stages)
@@ -926,7 +976,7 @@ int op_tiles(const Grid& g) {
 }
 
 size_t op_smem(int /*mode*/) {
-  return sizeof(double) * ((size_t)NS * STAGE + 18 * NT + 168) + sizeof(uint64_t) * NS + 16;
+  return sizeof(double) * ((size_t)NS * STAGE + (6 + GSN) * NT + 168) + sizeof(uint64_t) * NS + 16;
 }
 
 static void op_attr() {

@@ -85,7 +85,10 @@ constexpr int OP_BY = TOMO_OP_BY;
 constexpr int OP_MINB = OP_BY >= 16 ? 1 : 2;  // resident blocks per SM the tile is sized for
 constexpr int OP_OX = 30;           // output nodes per tile along x (even: 16-B TMA rows)
 constexpr int OP_OY = OP_BY - 1;    // output nodes per tile along y
-constexpr int OP_NS = 2;            // TMA pipeline stages (node planes in flight)
+#ifndef TOMO_OP_NS
+#define TOMO_OP_NS 2
+#endif
+constexpr int OP_NS = TOMO_OP_NS;   // TMA pipeline stages (node planes in flight)
 #ifndef TOMO_OP_PF
 #define TOMO_OP_PF 0
 #endif
