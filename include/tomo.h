@@ -166,6 +166,21 @@ int tomo_evaluate(tomo_ctx* ctx, const double* d_rho, double* d_u, double* d_dc,
 int tomo_evaluate_host(tomo_ctx* ctx, const double* h_rho, double* h_u, double* h_dcf,
                        double tol, int max_iters, double* c_out, tomo_solve_info* info);
 
+/* ---------------------------------------------------------------- two-scale coarse path
+ * ("coarse-grained design variable vector z_C ... each of
+ * its component is the averaged value of z in each subset", l.184-186 "3D blocks of
+ * uniform dimensions N_B x N_B x N_B ... K_C(z_C)u_C - f_C = 0", Alg. 1 lines 3-4;
+ * SPEC.md l.364-391). nb must divide nelx, nely and nelz (else TOMO_EINVAL).
+ * tomo_create_coarse: host-only; a new context for the coarse problem: grid nelx/nb x nely/nb x nelz/nb, edge
+ * nb*h, the fine material, and the fine BCs restricted per SPEC.md l.374-382 (reading R4):
+ * a coarse DOF is fixed iff a fine node whose nearest coarse node it is (per axis
+ * I = floor(i/nb + 1/2)) has that DOF fixed; fine loads are summed onto that node. The
+ * result is solved with the ordinary tomo_solve on its own bound workspace.
+ * tomo_coarsen: z_C[b] = mean of z over block b (element order on both grids), on the fine
+ * context's stream; d_z: N_e fine, d_zc: N_e / nb^3.                                    */
+int tomo_create_coarse(tomo_ctx** out, const tomo_ctx* fine, int nb);
+int tomo_coarsen(tomo_ctx* fine, const double* d_z, int nb, double* d_zc, int64_t n_ec);
+
 /* ---------------------------------------------------------------- introspection (tests)
  * Integer tables produced by the same device index code the kernels use, for bit-exact
  * parity with the oracle (BASELINE.json north_star: "DOF maps, filter neighbour lists,

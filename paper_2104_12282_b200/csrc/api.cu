@@ -927,3 +927,49 @@ extern "C" int tomo_bench_apply(tomo_ctx* c, const double* d_rho, int reps, doub
   if (ms_out) *ms_out = ms / reps;
   return TOMO_OK;
 }
+
+// ====================================================================== two-scale coarse path
+extern "C" int tomo_create_coarse(tomo_ctx** out, const tomo_ctx* f, int nb) {
+  if (!out || !f) return TOMO_EINVAL;
+  *out = nullptr;
+  const Grid& g = f->g;
+  if (nb < 1 || g.nx % nb || g.ny % nb || g.nz % nb) return TOMO_EINVAL;
+  const int cx = g.nx / nb, cy = g.ny / nb, cz = g.nz / nb;
+  // per-axis nearest coarse index, ties up (reading R4): I = floor((2 i + nb) / (2 nb))
+  auto near = [nb](int i) { return (2 * i + nb) / (2 * nb); };
+  auto cnode = [&](long long n) {
+    const int i = (int)(n % g.nnx), j = (int)((n / g.nnx) % g.nny), k = (int)(n / ((long long)g.nnx * g.nny));
+    return (long long)near(i) + (long long)(cx + 1) * (near(j) + (long long)(cy + 1) * near(k));
+  };
+  const long long nnc = (long long)(cx + 1) * (cy + 1) * (cz + 1);
+  std::vector<uint8_t> mc((size_t)nnc, 0);
+  for (long long n = 0; n < g.nn; ++n)
+    if (f->mask[n]) mc[cnode(n)] |= f->mask[n];
+  std::vector<int64_t> fixed;
+  for (long long n = 0; n < nnc; ++n)
+    for (int c = 0; c < 3; ++c)
+      if ((mc[n] >> c) & 1) fixed.push_back(3 * n + c);
+  std::vector<double> fc((size_t)(3 * nnc), 0.0);
+  for (size_t l = 0; l < f->load_dofs.size(); ++l) {
+    const int64_t d = f->load_dofs[l];
+    fc[3 * cnode(d / 3) + d % 3] += f->load_vals[l];
+  }
+  std::vector<int64_t> ld;
+  std::vector<double> lv;
+  for (long long d = 0; d < 3 * nnc; ++d)
+    if (fc[d] != 0.0) { ld.push_back(d); lv.push_back(fc[d]); }
+  tomo_grid gc{cx, cy, cz, f->h * nb};
+  tomo_bc bc{TOMO_BC_EXPLICIT, 0.0, fixed.data(), (int64_t)fixed.size(), ld.data(), lv.data(),
+             (int64_t)ld.size()};
+  return tomo_create(out, &gc, f->E0, f->Emin, f->nu, f->penal, f->rmin, &bc);
+}
+
+extern "C" int tomo_coarsen(tomo_ctx* c, const double* d_z, int nb, double* d_zc, int64_t n_ec) {
+  if (int rc = need_bound(c)) return rc;
+  const Grid& g = c->g;
+  if (nb < 1 || g.nx % nb || g.ny % nb || g.nz % nb) return fail(c, TOMO_EINVAL, "nb must divide the grid (SPEC.md l.386)");
+  if (n_ec != (int64_t)(g.nx / nb) * (g.ny / nb) * (g.nz / nb)) return fail(c, TOMO_ESIZE, "length mismatch");
+  if (!check_ptr(d_z) || !check_ptr(d_zc)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  LAUNCH(c, launch_coarsen(g, nb, d_z, d_zc, c->st));
+  return TOMO_OK;
+}

@@ -46,6 +46,11 @@ constexpr int VB_W = 3 * (OX + 2) + 2; // 98 doubles: vector rows (start offset 
 constexpr int DB_W = OX + 4;           // 34 doubles: Jacobi rows (start offset 0..1)
 constexpr int MB_W = 48;               // 48 bytes: mask rows (start offset 0..15)
 constexpr int E_W = 32;                // element box width (start offset 0..1, 31 used)
+#ifdef TOMO_FS
+constexpr int FSN = 12;                // lower face carried in shared memory
+#else
+constexpr int FSN = 0;                 // lower face recomputed from the last plane's nodes
+#endif
 #ifdef TOMO_GS6
 constexpr int GSN = 6;                 // top face carried as node sums
 #else
@@ -340,7 +345,12 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
   double* stages = smem;                     // [NS][STAGE]
   double* CD = stages + NS * STAGE;          // [2][3][NT] bottom-face contributions (by parity)
   double* GS = CD + 6 * NT;                  // [GSN][NT] thread-private: top face of the last element
+#ifdef TOMO_FS
+  double* FS = GS + GSN * NT;                // [12][NT] thread-private: face of the last plane
+  double* red = FS + 12 * NT;                // [168]
+#else
   double* red = GS + GSN * NT;               // [168]
+#endif
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 168);  // [NS]
   int* s_flag = reinterpret_cast<int*>(bars + NS);
 
@@ -488,6 +498,20 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
 
     // ---- element row ty between node rows b and o (lane 31's results are never read)
     double cup[3] = {0.0, 0.0, 0.0};
+#ifdef TOMO_FS
+    // face of this plane, kept in thread-private shared memory for the next plane
+    double Fn[12];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double bn = __shfl_down_sync(0xffffffffu, vb[c], 1);
+      const double on = __shfl_down_sync(0xffffffffu, vo[c], 1);
+      face_from(vb[c], bn, vo[c], on, Fn, c);
+    }
+    if (it >= 1) {
+      double Fc[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) Fc[i] = FS[i * NT + t];
+#else
     if (it >= 1) {
       double Fc[12], Fn[12];
 #pragma unroll
@@ -499,6 +523,7 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
         face_from(vb[c], bn, vo[c], on, Fn, c);
         face_from(vb_p[c], bnp, vo_p[c], onp, Fc, c);
       }
+#endif
       double Gb[12], Gt[12];
 #ifdef TOMO_EXP_NO_CORE  // timing experiment only: bypass the element core
 #pragma unroll
@@ -542,6 +567,10 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
 #pragma unroll
       for (int i = 0; i < 12; ++i) GS[i * NT + t] = Gt[i];
     }
+#endif
+#ifdef TOMO_FS
+#pragma unroll
+    for (int i = 0; i < 12; ++i) FS[i * NT + t] = Fn[i];
 #endif
     __syncthreads();  // CD of this plane complete; stage s consumed by every warp
     if (t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
@@ -909,6 +938,24 @@ __global__ void __launch_bounds__(256) k_oc(int ne, const double* __restrict__ x
   }
 }
 
+// ------------------------------------------------------------------ two-scale coarse path
+// z_C[b] = mean of z over the nb^3 fine elements of block b (fixed summation order k, j, i)
+__global__ void k_coarsen(Grid g, int nb, const double* __restrict__ z, double* __restrict__ zc) {
+  const int cx = g.nx / nb, cy = g.ny / nb;
+  const long long nc = (long long)cx * cy * (g.nz / nb);
+  const double inv = 1.0 / ((double)nb * nb * nb);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nc; b += stride) {
+    const int I = (int)(b % cx), J = (int)((b / cx) % cy), K = (int)(b / ((long long)cx * cy));
+    double s = 0.0;
+    for (int k = K * nb; k < K * nb + nb; ++k)
+      for (int j = J * nb; j < J * nb + nb; ++j)
+        for (int i = I * nb; i < I * nb + nb; ++i)
+          s += z[i + (long long)g.nx * (j + (long long)g.ny * k)];
+    zc[b] = s * inv;
+  }
+}
+
 // ------------------------------------------------------------------ introspection, bench
 __global__ void k_edofs(Grid g, long long* map) {
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -976,7 +1023,7 @@ int op_tiles(const Grid& g) {
 }
 
 size_t op_smem(int /*mode*/) {
-  return sizeof(double) * ((size_t)NS * STAGE + (6 + GSN) * NT + 168) + sizeof(uint64_t) * NS + 16;
+  return sizeof(double) * ((size_t)NS * STAGE + (6 + GSN + FSN) * NT + 168) + sizeof(uint64_t) * NS + 16;
 }
 
 static void op_attr() {
@@ -1111,6 +1158,11 @@ cudaError_t launch_mask_dofs(const Grid& g, const uint8_t* mask, uint8_t* out,
 cudaError_t launch_dinv_dense(const Grid& g, const double* dinv_pad, double* out,
                               cudaStream_t st) {
   k_dinv_dense<<<nblk(g.nn, 256, 148 * 16), 256, 0, st>>>(g, dinv_pad, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_coarsen(const Grid& g, int nb, const double* z, double* zc, cudaStream_t st) {
+  const long long nc = (long long)(g.nx / nb) * (g.ny / nb) * (g.nz / nb);
+  k_coarsen<<<nblk(nc, 256, 148 * 16), 256, 0, st>>>(g, nb, z, zc);
   return cudaGetLastError();
 }
 cudaError_t launch_dfma(double* out, int blocks, int iters, cudaStream_t st) {

@@ -159,6 +159,7 @@ cudaError_t launch_mask_dofs(const Grid& g, const uint8_t* mask, uint8_t* out,
                              cudaStream_t st);
 cudaError_t launch_dinv_dense(const Grid& g, const double* dinv_pad, double* out,
                               cudaStream_t st);
+cudaError_t launch_coarsen(const Grid& g, int nb, const double* z, double* zc, cudaStream_t st);
 cudaError_t launch_dfma(double* out, int blocks, int iters, cudaStream_t st);
 
 }  // namespace tomo

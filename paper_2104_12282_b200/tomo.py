@@ -94,6 +94,8 @@ _SIGS = [
     ("tomo_set_profiling", C.c_int, [C.c_void_p, C.c_int]),
     ("tomo_profile_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("tomo_bench_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_double)]),
+    ("tomo_create_coarse", C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int]),
+    ("tomo_coarsen", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64]),
 ]
 EXPORTS = [s[0] for s in _SIGS]
 
@@ -153,13 +155,16 @@ class Params:
 class Tomo:
     """One problem context bound to a torch-allocated workspace on the current device/stream."""
 
-    def __init__(self, p: Params, device: str | torch.device = "cuda", stream=None):
+    def __init__(self, p: Params, device: str | torch.device = "cuda", stream=None, _handle=None):
         lib = load_library()
         if not torch.cuda.is_available():
             raise RuntimeError("libtomo needs a CUDA device (no CPU fallback)")
         self.lib = lib
         self.p = p
         self.device = torch.device(device)
+        if _handle is not None:  # context already created (tomo_create_coarse)
+            self._bind(_handle, stream)
+            return
         g = _Grid(p.nelx, p.nely, p.nelz, p.h)
         fixed = (C.c_int64 * max(1, len(p.fixed_dofs)))(*p.fixed_dofs)
         ldofs = (C.c_int64 * max(1, len(p.load_dofs)))(*p.load_dofs)
@@ -175,6 +180,11 @@ class Tomo:
                 lib.tomo_destroy(h)
                 self.h = C.c_void_p()
             raise TomoError(rc, msg)
+        self._bind(h, stream)
+
+    def _bind(self, h, stream):
+        lib = self.lib
+        self.h = h
         sz = (C.c_int64 * 5)()
         lib.tomo_sizes(h, sz)
         self.n_e, self.n_n, self.n_dof, self.n_loads, self.n_taps = (int(v) for v in sz)
@@ -287,6 +297,27 @@ class Tomo:
                                                 C.c_void_p(dcf_h.data_ptr()), tol, max_iters,
                                                 C.byref(c), C.byref(info)))
         return c.value, info
+
+    # ------------------------------------------------------------------ two-scale coarse path
+    def coarse(self, nb: int) -> "Tomo":
+        """Context of the coarse problem K_C(z_C) u_C = f_C (tomo_create_coarse)."""
+        h = C.c_void_p()
+        rc = self.lib.tomo_create_coarse(C.byref(h), self.h, nb)
+        if rc != 0:
+            if h.value:
+                self.lib.tomo_destroy(h)
+            raise TomoError(rc, "tomo_create_coarse failed (nb must divide the grid)")
+        p = self.p
+        cp = Params(p.nelx // nb, p.nely // nb, p.nelz // nb, E0=p.E0, Emin=p.Emin, nu=p.nu,
+                    penal=p.penal, rmin=p.rmin, h=p.h * nb, bc=TOMO_BC_EXPLICIT)
+        return Tomo(cp, device=self.device, stream=self.stream, _handle=h)
+
+    def coarsen(self, z: torch.Tensor, nb: int, out: torch.Tensor | None = None):
+        n_ec = (self.p.nelx // nb) * (self.p.nely // nb) * (self.p.nelz // nb)
+        out = torch.zeros(n_ec, dtype=torch.float64, device=self.device) if out is None else out
+        self._check(self.lib.tomo_coarsen(self.h, _ptr(_f64(z, self.n_e, "z")), nb,
+                                          _ptr(_f64(out, n_ec, "zc")), n_ec))
+        return out
 
     # ------------------------------------------------------------------ introspection
     def ke(self):

@@ -136,3 +136,32 @@ def test_workspace_fits_hbm_at_largest_config(lib):
     assert rc == 0
     assert lib.tomo_workspace_bytes(hnd) < 2 * 1024 ** 3  # < 2 GB of 180 GB HBM
     lib.tomo_destroy(hnd)
+
+
+@pytest.mark.parametrize("dims,bc,nb", [((8, 4, 4), 1, 2), ((24, 12, 12), 1, 4), ((12, 8, 8), 2, 2),
+                                        ((6, 3, 3), 1, 3), ((5, 3, 7), 1, 1)])
+def test_coarse_context_loads_match_oracle_restriction(lib, dims, bc, nb):
+    """tomo_create_coarse (host-only) vs oracle.twoscale.restrict_bc: load DOFs bit-exact,
+    values to rounding, sizes by the SPEC.md l.386 rule."""
+    from oracle import twoscale
+    rc, fine = _create(lib, *dims, bc=bc)
+    assert rc == 0
+    coarse = C.c_void_p()
+    assert lib.tomo_create_coarse(C.byref(coarse), fine, nb) == 0
+    sz = (C.c_int64 * 5)()
+    lib.tomo_sizes(coarse, sz)
+    assert tuple(sz[:3]) == grid.counts(*(d // nb for d in dims))
+    n = C.c_int64(0)
+    lib.tomo_get_load(coarse, None, None, C.byref(n))
+    d = (C.c_int64 * max(1, n.value))()
+    v = (C.c_double * max(1, n.value))()
+    lib.tomo_get_load(coarse, d, v, C.byref(n))
+    fixed, ld, lv = grid.bc_for(bc, *dims)
+    fc, ldc, lvc = twoscale.restrict_bc(*dims, nb, fixed, ld, lv)
+    order = np.argsort(np.array(d[:n.value]))
+    assert np.array_equal(np.array(d[:n.value])[order], ldc)
+    assert np.allclose(np.array(v[:n.value])[order], lvc, rtol=1e-15, atol=0)
+    bad = C.c_void_p()
+    assert lib.tomo_create_coarse(C.byref(bad), fine, 7) == -1  # 7 divides none of the grids
+    lib.tomo_destroy(coarse)
+    lib.tomo_destroy(fine)
