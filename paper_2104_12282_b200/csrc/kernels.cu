@@ -370,9 +370,18 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
   // persistent, balanced schedule: block b owns work units [ub, ue) of the list
   // (tile, node plane), tile-major; it processes them as z-segments split at tile edges
   const int tiles_x = (g.nnx + OX - 1) / OX;
-  const long long units = (long long)a.ntiles * g.nnz;
-  const int ub = (int)((units * blockIdx.x) / gridDim.x);
-  const int ue = (int)((units * (blockIdx.x + 1)) / gridDim.x);
+  int ub, ue;
+  if (a.zchunks > 0) {
+    // synchronised schedule: block = (tile, z-chunk), equal chunks, so every block marches
+    // the same planes at the same time and neighbouring tiles share their halos through L2
+    const int tile = blockIdx.x % a.ntiles, ch = blockIdx.x / a.ntiles;
+    ub = tile * g.nnz + (ch * g.nnz) / a.zchunks;
+    ue = tile * g.nnz + ((ch + 1) * g.nnz) / a.zchunks;
+  } else {
+    const long long units = (long long)a.ntiles * g.nnz;
+    ub = (int)((units * blockIdx.x) / gridDim.x);
+    ue = (int)((units * (blockIdx.x + 1)) / gridDim.x);
+  }
 
   if (t == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);

@@ -113,7 +113,8 @@ struct OpArgs {
   double* out;          // APPLY: y (raw u at fixed DOFs) ; PCG: q
   double* partials;     // PCG: five per block
   Scal* s;              // PCG
-  int ntiles;           // x-y tiles; the grid is persistent (1-D, balanced)
+  int ntiles;           // x-y tiles
+  int zchunks;          // 0: persistent balanced schedule; > 0: block = (tile, z-chunk)
   unsigned long long cond;  // PCG in a CUDA graph: WHILE-node handle cleared when done (0: none)
 };
 
