@@ -181,6 +181,24 @@ int tomo_evaluate_host(tomo_ctx* ctx, const double* h_rho, double* h_u, double* 
 int tomo_create_coarse(tomo_ctx** out, const tomo_ctx* fine, int nb);
 int tomo_coarsen(tomo_ctx* fine, const double* d_z, int nb, double* d_zc, int64_t n_ec);
 
+/* ---------------------------------------------------------------- multigrid-preconditioned CG
+ * ("Iterative solvers such as preconditioned conjugate
+ * gradient (PCG) and multi-grid methods are typically used"). Optional solver; the metric
+ * path is the Jacobi-PCG of tomo_solve. Levels l = 1..levels-1 halve the grid (each
+ * dimension must be divisible by 2^(levels-1)); their E is the mean of the 8 children's E,
+ * their BCs those of tomo_create_coarse(nb = 2). Preconditioner: one V-cycle with `nu`
+ * damped-Jacobi sweeps (weight omega) before and after the coarse correction, full-weighting
+ * restriction = transpose of trilinear prolongation, the coarsest level solved by the fused
+ * Jacobi-PCG to coarse_tol (at most coarse_iters). Outer loop: flexible CG (Polak-Ribiere
+ * beta) from x0 = 0, stopped on ||r_k|| <= tol ||f||; returns iterations >= 0 or a status.
+ * tomo_mg_workspace_bytes is host-only (builds the level contexts); tomo_mg_bind binds a
+ * caller-owned device workspace of that size (256-B aligned) on the context's stream.     */
+size_t tomo_mg_workspace_bytes(tomo_ctx* ctx, int levels);
+int tomo_mg_bind(tomo_ctx* ctx, int levels, void* d_workspace, size_t bytes);
+int tomo_mg_params(tomo_ctx* ctx, int nu, double omega, int coarse_iters, double coarse_tol);
+int tomo_solve_mg(tomo_ctx* ctx, const double* d_rho, int64_t n_e, double* d_u, int64_t n_dof,
+                  double tol, int max_iters, tomo_solve_info* info);
+
 /* ---------------------------------------------------------------- introspection (tests)
  * Integer tables produced by the same device index code the kernels use, for bit-exact
  * parity with the oracle (BASELINE.json north_star: "DOF maps, filter neighbour lists,

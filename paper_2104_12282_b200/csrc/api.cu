@@ -53,6 +53,19 @@ struct tomo_ctx {
   OpArgs op_apply_u{}, op_apply_p0{}, op_pcg[2];  // op_pcg[k & 1] for launch k
   cudaGraph_t pcg_graph = nullptr;        // WHILE(not done) { launch even; launch odd }
   cudaGraphExec_t pcg_exec = nullptr;
+  // multigrid hierarchy (tomo_mg_*): levels 1..L-1 are coarse contexts bound to the caller's
+  // MG workspace; the outer flexible-CG vectors of the fine level live there too
+  std::vector<tomo_ctx*> mg;
+  char* mg_ws = nullptr;
+  size_t mg_off_U = 0, mg_off_R = 0, mg_off_P = 0, mg_off_Q = 0, mg_off_Z = 0, mg_off_Zo = 0,
+         mg_off_part = 0, mg_end = 0;
+  std::vector<size_t> mg_level_off;
+  OpArgs op_apply_P{}, op_apply_Z{};
+  bool mg_bound = false;
+  int mg_nu = 2;              // pre- and post-smoothing sweeps
+  double mg_omega = 0.6;      // damped Jacobi
+  int mg_coarse_iters = 200;  // coarsest level: fused Jacobi-PCG, loose tolerance
+  double mg_coarse_tol = 1e-3;
   // profiling
   bool prof = false;
   double prof_a_ms = 0, prof_b_ms = 0;
@@ -407,6 +420,7 @@ extern "C" size_t tomo_workspace_bytes(const tomo_ctx* c) { return c ? c->off_en
 
 extern "C" void tomo_destroy(tomo_ctx* c) {
   if (!c) return;
+  for (auto* l : c->mg) tomo_destroy(l);
   if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
   if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
   for (auto e : c->ev) cudaEventDestroy(e);
@@ -598,19 +612,11 @@ int prepare_modulus(tomo_ctx* c, const double* d_rho, bool jacobi) {
   return TOMO_OK;
 }
 
-// Single-pass Jacobi-PCG on the bound workspace (DESIGN.md §5.3): E / dinv ready; c->u()
-// holds x0 (padded, masked). One fused launch per iteration; launch k checks r_k.
-int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) {
-  const Grid& g = c->g;
-  const int nl = (int)c->load_dofs.size();
-  const size_t vb = sizeof(double) * (size_t)g.ndof_pad;
-  Scal hs{};
-  LAUNCH(c, launch_scal_init(c->scal(), tol * c->fnorm, max_iters, c->st));
-  // r_{-1} := r0 = f - K u0 in r[1]; q_{-1} = p_{-1} = 0
-  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));
-  LAUNCH(c, launch_resid(g, c->q(0), c->r(1), c->ldp(), c->lv(), nl, c->st));
-  CK(c, cudaMemsetAsync(c->q(1), 0, vb, c->st));
-  CK(c, cudaMemsetAsync(c->p(1), 0, vb, c->st));
+// The PCG launches (graph or host batches) until the device sets `done`; *hs_out = final
+// scalars. The scalars, r_{-1}, q_{-1}, p_{-1} and u must be initialised by the caller.
+int run_pcg_loop(tomo_ctx* c, int max_iters, Scal* hs_out) {
+  Scal& hs = *hs_out;
+  hs = Scal{};
   int k = 0;  // launches issued
   int batch = 8;
   const bool prof = c->prof;
@@ -654,6 +660,23 @@ int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) 
     if (batch < 128) batch *= 2;
   }
   }
+  return TOMO_OK;
+}
+
+// Single-pass Jacobi-PCG on the bound workspace (DESIGN.md §5.3): E / dinv ready; c->u()
+// holds x0 (padded, masked). One fused launch per iteration; launch k checks r_k.
+int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) {
+  const Grid& g = c->g;
+  const int nl = (int)c->load_dofs.size();
+  const size_t vb = sizeof(double) * (size_t)g.ndof_pad;
+  Scal hs{};
+  LAUNCH(c, launch_scal_init(c->scal(), tol * c->fnorm, max_iters, c->st));
+  // r_{-1} := r0 = f - K u0 in r[1]; q_{-1} = p_{-1} = 0
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));
+  LAUNCH(c, launch_resid(g, c->q(0), c->r(1), c->ldp(), c->lv(), nl, c->st));
+  CK(c, cudaMemsetAsync(c->q(1), 0, vb, c->st));
+  CK(c, cudaMemsetAsync(c->p(1), 0, vb, c->st));
+  if (int rc = run_pcg_loop(c, max_iters, &hs)) return rc;
   if (hs.done == 3) {
     return fail(c, hs.status ? hs.status : TOMO_EBREAKDOWN,
                 hs.status == TOMO_ENAN ? "NaN/Inf in PCG" : "PCG breakdown: p^T K p <= 0 (SPEC.md l.173)");
@@ -989,5 +1012,249 @@ extern "C" int tomo_coarsen(tomo_ctx* c, const double* d_z, int nb, double* d_zc
   if (n_ec != (int64_t)(g.nx / nb) * (g.ny / nb) * (g.nz / nb)) return fail(c, TOMO_ESIZE, "length mismatch");
   if (!check_ptr(d_z) || !check_ptr(d_zc)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
   LAUNCH(c, launch_coarsen(g, nb, d_z, d_zc, c->st));
+  return TOMO_OK;
+}
+
+// ====================================================================== multigrid
+namespace {
+
+int mg_levels_possible(const Grid& g) {
+  int L = 1;
+  int x = g.nx, y = g.ny, z = g.nz;
+  while (x % 2 == 0 && y % 2 == 0 && z % 2 == 0 && x >= 2 && y >= 2 && z >= 2) {
+    x /= 2; y /= 2; z /= 2;
+    ++L;
+  }
+  return L;
+}
+
+// APPLY with an arbitrary (padded, fine-level) input buffer: maps built at tomo_mg_bind
+int mg_build_maps(tomo_ctx* c) {
+  const Grid& g = c->g;
+  const uint64_t rowv = 24ull * g.nnx_pad, planev = rowv * g.nny;
+  const uint32_t inw = 3 * (OP_OX + 2) + 2, inh = OP_BY + 1;
+  CUtensorMap tP, tZ;
+  auto P = [&](size_t off) { return reinterpret_cast<double*>(c->mg_ws + off); };
+  if (int rc = make_map(c, &tP, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, P(c->mg_off_P), 3ull * g.nnx, g.nny, g.nnz, rowv, planev, inw, inh)) return rc;
+  if (int rc = make_map(c, &tZ, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, P(c->mg_off_Z), 3ull * g.nnx, g.nny, g.nnz, rowv, planev, inw, inh)) return rc;
+  c->op_apply_P = c->op_apply_u;
+  c->op_apply_P.tm_in = tP;
+  c->op_apply_P.out = P(c->mg_off_Q);
+  c->op_apply_Z = c->op_apply_u;
+  c->op_apply_Z.tm_in = tZ;
+  c->op_apply_Z.out = c->q(0);
+  return TOMO_OK;
+}
+
+double* mgv(tomo_ctx* c, size_t off) { return reinterpret_cast<double*>(c->mg_ws + off); }
+
+// PCG on context c with the right-hand side already in r(1) (padded): relative tolerance
+// tol on ||b||, from u = 0. The coarsest level of the V-cycle.
+int pcg_rhs(tomo_ctx* c, double tol, int max_iters, int* iters) {
+  const Grid& g = c->g;
+  const size_t vb = sizeof(double) * (size_t)g.ndof_pad;
+  LAUNCH(c, launch_scal_init(c->scal(), 0.0, max_iters, c->st));
+  LAUNCH(c, launch_norm2(g, c->r(1), c->scal(), c->part(), c->nb_b, c->st));
+  LAUNCH(c, launch_set_tol(c->scal(), tol, c->st));
+  CK(c, cudaMemsetAsync(c->u(), 0, vb, c->st));
+  CK(c, cudaMemsetAsync(c->q(1), 0, vb, c->st));
+  CK(c, cudaMemsetAsync(c->p(1), 0, vb, c->st));
+  Scal hs{};
+  if (int rc = run_pcg_loop(c, max_iters, &hs)) return rc;
+  if (hs.done == 3 && hs.status != TOMO_EBREAKDOWN) return fail(c, hs.status ? hs.status : TOMO_ENAN, "NaN in the coarse solve");
+  if (iters) *iters = hs.iters;
+  return TOMO_OK;
+}
+
+// x = V-cycle(b) on level l (l = 0: the fine context with outer buffers b = R, x = Z).
+int mg_vcycle(tomo_ctx* f, int l, const double* b, double* x) {
+  tomo_ctx* c = l == 0 ? f : f->mg[l - 1];
+  const Grid& g = c->g;
+  const int L = (int)f->mg.size() + 1;
+  const size_t vb = sizeof(double) * (size_t)g.ndof_pad;
+  if (l == L - 1) {  // coarsest: approximate solve by Jacobi-PCG
+    if (b != c->r(1)) CK(c, cudaMemcpyAsync(c->r(1), b, vb, cudaMemcpyDeviceToDevice, c->st));
+    int it = 0;
+    if (int rc = pcg_rhs(c, f->mg_coarse_tol, f->mg_coarse_iters, &it)) return rc;
+    if (x != c->u()) CK(c, cudaMemcpyAsync(x, c->u(), vb, cudaMemcpyDeviceToDevice, c->st));
+    return TOMO_OK;
+  }
+  const OpArgs& ax = l == 0 ? f->op_apply_Z : c->op_apply_u;  // K x -> c->q(0)
+  const double om = f->mg_omega;
+  // pre-smoothing from x = 0: the first sweep is x = omega D^-1 b
+  CK(c, cudaMemsetAsync(x, 0, vb, c->st));
+  CK(c, cudaMemsetAsync(c->q(0), 0, vb, c->st));
+  for (int s = 0; s < f->mg_nu; ++s) {
+    if (s > 0) LAUNCH(c, launch_op(OP_APPLY, ax, c->op_blocks, c->st));
+    LAUNCH(c, launch_jacobi_smooth(g, om, b, c->q(0), c->dinv(), c->dmask(), x, c->st));
+  }
+  // residual, restriction, coarse correction, prolongation
+  tomo_ctx* n = f->mg[l];
+  LAUNCH(c, launch_op(OP_APPLY, ax, c->op_blocks, c->st));
+  LAUNCH(c, launch_residual(g, b, c->q(0), c->dmask(), c->r(1), c->st));
+  const bool coarsest_next = (l + 1 == L - 1);
+  double* bn = coarsest_next ? n->r(1) : n->r(0);
+  LAUNCH(c, launch_restrict(g, n->g, c->r(1), n->dmask(), bn, c->st));
+  if (int rc = mg_vcycle(f, l + 1, bn, n->u())) return rc;
+  LAUNCH(c, launch_prolong_add(g, n->g, n->u(), c->dmask(), x, c->st));
+  // post-smoothing (same sweeps: symmetric cycle)
+  for (int s = 0; s < f->mg_nu; ++s) {
+    LAUNCH(c, launch_op(OP_APPLY, ax, c->op_blocks, c->st));
+    LAUNCH(c, launch_jacobi_smooth(g, om, b, c->q(0), c->dinv(), c->dmask(), x, c->st));
+  }
+  return TOMO_OK;
+}
+
+// host sum of the dot3 block partials in block order (deterministic)
+int mg_dot3(tomo_ctx* f, const double* a, const double* b, const double* c3, double out[3]) {
+  const int nb = f->sms * 4;
+  LAUNCH(f, launch_dot3(f->g.ndof_pad, a, b, c3, mgv(f, f->mg_off_part), nb, f->st));
+  std::vector<double> h((size_t)3 * nb);
+  CK(f, cudaMemcpyAsync(h.data(), mgv(f, f->mg_off_part), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, f->st));
+  CK(f, cudaStreamSynchronize(f->st));
+  out[0] = out[1] = out[2] = 0.0;
+  for (int i = 0; i < nb; ++i) {
+    out[0] += h[3 * i];
+    out[1] += h[3 * i + 1];
+    out[2] += h[3 * i + 2];
+  }
+  return TOMO_OK;
+}
+
+}  // namespace
+
+extern "C" size_t tomo_mg_workspace_bytes(tomo_ctx* c, int levels) {
+  if (!c || levels < 2 || levels > mg_levels_possible(c->g)) return 0;
+  if ((int)c->mg.size() != levels - 1) {
+    for (auto* l : c->mg) tomo_destroy(l);
+    c->mg.clear();
+    c->mg_bound = false;
+    const tomo_ctx* prev = c;
+    for (int l = 1; l < levels; ++l) {
+      tomo_ctx* n = nullptr;
+      if (tomo_create_coarse(&n, prev, 2) != TOMO_OK) {
+        if (n) tomo_destroy(n);
+        for (auto* x : c->mg) tomo_destroy(x);
+        c->mg.clear();
+        return 0;
+      }
+      c->mg.push_back(n);
+      prev = n;
+    }
+  }
+  size_t o = 0;
+  c->mg_level_off.clear();
+  for (auto* l : c->mg) {
+    c->mg_level_off.push_back(o);
+    o = align_up(o + l->off_end);
+  }
+  const size_t vp = sizeof(double) * (size_t)c->g.ndof_pad;
+  c->mg_off_U = o; o = align_up(o + vp);
+  c->mg_off_R = o; o = align_up(o + vp);
+  c->mg_off_P = o; o = align_up(o + vp);
+  c->mg_off_Q = o; o = align_up(o + vp);
+  c->mg_off_Z = o; o = align_up(o + vp);
+  c->mg_off_Zo = o; o = align_up(o + vp);
+  c->mg_off_part = o; o = align_up(o + sizeof(double) * 3 * 4 * 1024);
+  c->mg_end = o;
+  return o;
+}
+
+extern "C" int tomo_mg_bind(tomo_ctx* c, int levels, void* d_ws, size_t bytes) {
+  if (int rc = need_bound(c)) return rc;
+  const size_t need = tomo_mg_workspace_bytes(c, levels);
+  if (!need) return fail(c, TOMO_EINVAL, "levels must be >= 2 and the grid divisible by 2^(levels-1)");
+  if (!d_ws || (reinterpret_cast<uintptr_t>(d_ws) & 255)) return fail(c, TOMO_EINVAL, "MG workspace must be 256-B aligned");
+  if (bytes < need) return fail(c, TOMO_ENOWORKSPACE, "MG workspace too small");
+  c->mg_ws = static_cast<char*>(d_ws);
+  CK(c, cudaMemsetAsync(c->mg_ws, 0, need, c->st));
+  for (size_t l = 0; l < c->mg.size(); ++l) {
+    if (int rc = tomo_bind(c->mg[l], c->mg_ws + c->mg_level_off[l], c->mg[l]->off_end, c->st))
+      return fail(c, rc, std::string("binding MG level: ") + tomo_last_error(c->mg[l]));
+  }
+  if (int rc = mg_build_maps(c)) return rc;
+  c->mg_bound = true;
+  return TOMO_OK;
+}
+
+extern "C" int tomo_solve_mg(tomo_ctx* c, const double* d_rho, int64_t n_e, double* d_u,
+                             int64_t n_dof, double tol, int max_iters, tomo_solve_info* info) {
+  if (int rc = need_bound(c)) return rc;
+  if (!c->mg_bound) return fail(c, TOMO_ENOWORKSPACE, "call tomo_mg_bind first");
+  if (n_e != c->g.ne || n_dof != c->g.ndof) return fail(c, TOMO_ESIZE, "length mismatch");
+  if (!check_ptr(d_rho) || !check_ptr(d_u)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
+  if (c->fnorm == 0.0) {
+    CK(c, cudaMemsetAsync(d_u, 0, sizeof(double) * (size_t)n_dof, c->st));
+    CK(c, cudaStreamSynchronize(c->st));
+    if (info) *info = tomo_solve_info{0, 1, 0.0, 0.0};
+    return 0;
+  }
+  const Grid& g = c->g;
+  const long long n = g.ndof_pad;
+  const size_t vb = sizeof(double) * (size_t)n;
+  if (int rc = prepare_modulus(c, d_rho, true)) return rc;
+  // coarse levels: E averaged over the 8 children, their own Jacobi diagonals
+  const tomo_ctx* prev = c;
+  for (auto* l : c->mg) {
+    LAUNCH(c, launch_coarsen_E(prev->g, l->g, prev->E(), l->E(), c->st));
+    LAUNCH(c, launch_jacobi(l->g, l->E(), l->ke_diag, l->dinv(), c->st));
+    prev = l;
+  }
+  double *U = mgv(c, c->mg_off_U), *R = mgv(c, c->mg_off_R), *Pv = mgv(c, c->mg_off_P),
+         *Q = mgv(c, c->mg_off_Q), *Z = mgv(c, c->mg_off_Z), *Zo = mgv(c, c->mg_off_Zo);
+  // x0 = 0, r0 = f (the flexible CG below runs from a cold start, reading A12)
+  CK(c, cudaMemsetAsync(U, 0, vb, c->st));
+  CK(c, cudaMemsetAsync(c->q(0), 0, vb, c->st));
+  LAUNCH(c, launch_resid(g, c->q(0), R, c->ldp(), c->lv(), (int)c->load_dofs.size(), c->st));
+  if (int rc = mg_vcycle(c, 0, R, Z)) return rc;
+  CK(c, cudaMemcpyAsync(Pv, Z, vb, cudaMemcpyDeviceToDevice, c->st));
+  double d[3];
+  if (int rc = mg_dot3(c, R, Z, nullptr, d)) return rc;
+  double rz = d[0], rr = d[2];
+  const double stop = tol * c->fnorm;
+  int k = 0;
+  bool conv = std::sqrt(rr) <= stop;
+  while (!conv && k < max_iters) {
+    LAUNCH(c, launch_op(OP_APPLY, c->op_apply_P, c->op_blocks, c->st));  // Q = K P
+    if (int rc = mg_dot3(c, Pv, Q, nullptr, d)) return rc;
+    const double pq = d[0];
+    if (!(pq > 0.0) || !std::isfinite(pq)) return fail(c, std::isnan(pq) ? TOMO_ENAN : TOMO_EBREAKDOWN, "MG-CG breakdown: p^T K p <= 0");
+    const double alpha = rz / pq;
+    LAUNCH(c, launch_axpy2(n, alpha, Pv, U, -alpha, Q, R, c->st));  // U += a P ; R -= a Q
+    ++k;
+    CK(c, cudaMemcpyAsync(Zo, Z, vb, cudaMemcpyDeviceToDevice, c->st));
+    if (int rc = mg_vcycle(c, 0, R, Z)) return rc;
+    if (int rc = mg_dot3(c, R, Z, Zo, d)) return rc;  // r.z, r.z_old, r.r
+    rr = d[2];
+    if (!std::isfinite(rr)) return fail(c, TOMO_ENAN, "NaN/Inf in MG-CG");
+    if (std::sqrt(rr) <= stop) { conv = true; break; }
+    const double beta = (d[0] - d[1]) / rz;  // flexible (Polak-Ribiere) beta
+    rz = d[0];
+    LAUNCH(c, launch_xpby(n, Z, beta, Pv, c->st));  // P = Z + beta P
+  }
+  // true residual, then u out
+  CK(c, cudaMemcpyAsync(c->u(), U, vb, cudaMemcpyDeviceToDevice, c->st));
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));
+  LAUNCH(c, launch_resid(g, c->q(0), c->r(0), c->ldp(), c->lv(), (int)c->load_dofs.size(), c->st));
+  LAUNCH(c, launch_norm2(g, c->r(0), c->scal(), c->part(), c->nb_b, c->st));
+  LAUNCH(c, launch_unpack(g, U, d_u, c->st));
+  double rrt = 0;
+  CK(c, cudaMemcpyAsync(&rrt, &c->scal()->rr_true, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  if (info) {
+    info->iterations = k;
+    info->converged = conv;
+    info->rel_res_recursive = std::sqrt(rr) / c->fnorm;
+    info->rel_res_true = std::sqrt(rrt) / c->fnorm;
+  }
+  return k;
+}
+
+extern "C" int tomo_mg_params(tomo_ctx* c, int nu, double omega, int coarse_iters, double coarse_tol) {
+  if (!c || nu < 1 || !(omega > 0 && omega < 2) || coarse_iters < 1 || !(coarse_tol > 0)) return TOMO_EINVAL;
+  c->mg_nu = nu;
+  c->mg_omega = omega;
+  c->mg_coarse_iters = coarse_iters;
+  c->mg_coarse_tol = coarse_tol;
   return TOMO_OK;
 }

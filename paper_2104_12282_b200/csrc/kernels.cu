@@ -1174,6 +1174,11 @@ cudaError_t launch_coarsen(const Grid& g, int nb, const double* z, double* zc, c
   k_coarsen<<<nblk(nc, 256, 148 * 16), 256, 0, st>>>(g, nb, z, zc);
   return cudaGetLastError();
 }
+__global__ void k_set_tol(Scal* s, double tol) { s->tol_fnorm = tol * sqrt(s->rr_true); }
+cudaError_t launch_set_tol(Scal* s, double tol, cudaStream_t st) {
+  k_set_tol<<<1, 1, 0, st>>>(s, tol);
+  return cudaGetLastError();
+}
 cudaError_t launch_dfma(double* out, int blocks, int iters, cudaStream_t st) {
   k_dfma<<<blocks, 256, 0, st>>>(out, iters);
   return cudaGetLastError();

@@ -1,0 +1,231 @@
+// libtomo multigrid kernels ("Iterative solvers such
+// as preconditioned conjugate gradient (PCG) and multi-grid methods are typically used").
+//
+// Geometric multigrid on the structured grid, used as the preconditioner of a flexible CG:
+//   level l+1 = level l coarsened by 2 per axis, element edge 2h, E averaged over the 8
+//   children (rediscretisation), BCs restricted by tomo_create_coarse (reading R4);
+//   V-cycle: damped Jacobi smoothing (the same operator kernel), full-weighting restriction
+//   R = P^T, trilinear prolongation P; fixed DOFs are zero in every correction.
+// All vectors are in the padded internal layout of their level (tomo_internal.h).
+#include "tomo_internal.h"
+
+namespace tomo {
+namespace {
+
+inline unsigned nblk(long long n, int bs, int cap) {
+  long long b = (n + bs - 1) / bs;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (unsigned)b;
+}
+
+__device__ __forceinline__ void node_of(const Grid& g, long long n, int& i, int& j, int& k) {
+  i = (int)(n % g.nnx);
+  j = (int)((n / g.nnx) % g.nny);
+  k = (int)(n / ((long long)g.nnx * g.nny));
+}
+
+// x += omega D^-1 (b - Kx) on free DOFs (Kx: the operator applied to x)
+__global__ void k_jacobi_smooth(Grid g, double omega, const double* __restrict__ b,
+                                const double* __restrict__ kx, const double* __restrict__ dinv,
+                                const uint8_t* __restrict__ mask, double* __restrict__ x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < g.nn; n += stride) {
+    int i, j, k;
+    node_of(g, n, i, j, k);
+    const long long p = 3 * node_pad(g, i, j, k);
+    const unsigned m = mask[mask_index(g, i, j, k)];
+    const double w = omega * dinv[node_pad(g, i, j, k)];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      x[p + c] = ((m >> c) & 1u) ? 0.0 : fma(w, b[p + c] - kx[p + c], x[p + c]);
+  }
+}
+
+// r = b - Kx on free DOFs (0 at fixed DOFs)
+__global__ void k_residual(Grid g, const double* __restrict__ b, const double* __restrict__ kx,
+                           const uint8_t* __restrict__ mask, double* __restrict__ r) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < g.nn; n += stride) {
+    int i, j, k;
+    node_of(g, n, i, j, k);
+    const long long p = 3 * node_pad(g, i, j, k);
+    const unsigned m = mask[mask_index(g, i, j, k)];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) r[p + c] = ((m >> c) & 1u) ? 0.0 : b[p + c] - kx[p + c];
+  }
+}
+
+// 1-D trilinear weight of fine index f for coarse index C (f = 2C + d, |d| <= 1)
+__device__ __forceinline__ double w1(int f, int C) {
+  const int d = f - 2 * C;
+  return d == 0 ? 1.0 : ((d == 1 || d == -1) ? 0.5 : 0.0);
+}
+
+// rc = P^T rf (full weighting: 27 fine nodes around 2C with weights prod (1 - |d|/2));
+// zero at coarse fixed DOFs. Fixed summation order dz, dy, dx.
+__global__ void k_restrict(Grid gf, Grid gc, const double* __restrict__ rf,
+                           const uint8_t* __restrict__ maskc, double* __restrict__ rc) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < gc.nn; n += stride) {
+    int I, J, K;
+    node_of(gc, n, I, J, K);
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int dz = -1; dz <= 1; ++dz) {
+      const int k = 2 * K + dz;
+      if (k < 0 || k > gf.nz) continue;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int j = 2 * J + dy;
+        if (j < 0 || j > gf.ny) continue;
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int i = 2 * I + dx;
+          if (i < 0 || i > gf.nx) continue;
+          const double w = w1(i, I) * w1(j, J) * w1(k, K);
+          const long long p = 3 * node_pad(gf, i, j, k);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) s[c] = fma(w, rf[p + c], s[c]);
+        }
+      }
+    }
+    const long long q = 3 * node_pad(gc, I, J, K);
+    const unsigned m = maskc[mask_index(gc, I, J, K)];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rc[q + c] = ((m >> c) & 1u) ? 0.0 : s[c];
+  }
+}
+
+// xf += P xc (trilinear interpolation from the coarse nodes around f/2); zero at fine fixed
+__global__ void k_prolong_add(Grid gf, Grid gc, const double* __restrict__ xc,
+                              const uint8_t* __restrict__ maskf, double* __restrict__ xf) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < gf.nn; n += stride) {
+    int i, j, k;
+    node_of(gf, n, i, j, k);
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int K = k >> 1; K <= (k + 1) >> 1; ++K) {
+      if (K > gc.nz) continue;
+      const double wz = w1(k, K);
+      for (int J = j >> 1; J <= (j + 1) >> 1; ++J) {
+        if (J > gc.ny) continue;
+        const double wy = wz * w1(j, J);
+        for (int I = i >> 1; I <= (i + 1) >> 1; ++I) {
+          if (I > gc.nx) continue;
+          const double w = wy * w1(i, I);
+          const long long q = 3 * node_pad(gc, I, J, K);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) s[c] = fma(w, xc[q + c], s[c]);
+        }
+      }
+    }
+    const long long p = 3 * node_pad(gf, i, j, k);
+    const unsigned m = maskf[mask_index(gf, i, j, k)];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) xf[p + c] = ((m >> c) & 1u) ? 0.0 : xf[p + c] + s[c];
+  }
+}
+
+// coarse E = mean of the 8 child elements' E (padded element layouts on both levels)
+__global__ void k_coarsen_E(Grid gf, Grid gc, const double* __restrict__ Ef, double* __restrict__ Ec) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < gc.ne; e += stride) {
+    const int I = (int)(e % gc.nx), J = (int)((e / gc.nx) % gc.ny), K = (int)(e / ((long long)gc.nx * gc.ny));
+    double s = 0.0;
+    for (int k = 2 * K; k < 2 * K + 2; ++k)
+      for (int j = 2 * J; j < 2 * J + 2; ++j)
+        for (int i = 2 * I; i < 2 * I + 2; ++i) s += Ef[elem_pad(gf, i, j, k)];
+    Ec[elem_pad(gc, I, J, K)] = 0.125 * s;
+  }
+}
+
+// ---- flexible-CG vector kernels (flat over padded vectors; pads are 0) -----------------
+__global__ void k_axpy2(long long n, double a, const double* __restrict__ x, double* __restrict__ y,
+                        double b, const double* __restrict__ z, double* __restrict__ w) {
+  // y += a x ; w += b z
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride) {
+    y[d] = fma(a, x[d], y[d]);
+    w[d] = fma(b, z[d], w[d]);
+  }
+}
+__global__ void k_xpby(long long n, const double* __restrict__ x, double b, double* __restrict__ y) {
+  // y = x + b y
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride)
+    y[d] = fma(b, y[d], x[d]);
+}
+
+// three dot products <a,b>, <a,c>, <a,a> in one pass: deterministic block partials
+__global__ void __launch_bounds__(256) k_dot3(long long n, const double* __restrict__ a,
+                                              const double* __restrict__ b,
+                                              const double* __restrict__ c, double* partials) {
+  __shared__ double red[3][8];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride) {
+    const double av = a[d];
+    s0 = fma(av, b[d], s0);
+    s1 = c ? fma(av, c[d], s1) : 0.0;
+    s2 = fma(av, av, s2);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = s0;
+    red[1][threadIdx.x >> 5] = s1;
+    red[2][threadIdx.x >> 5] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
+    partials[3 * blockIdx.x + threadIdx.x] = t;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_jacobi_smooth(const Grid& g, double omega, const double* b, const double* kx,
+                                 const double* dinv, const uint8_t* mask, double* x, cudaStream_t st) {
+  k_jacobi_smooth<<<nblk(g.nn, 256, 148 * 16), 256, 0, st>>>(g, omega, b, kx, dinv, mask, x);
+  return cudaGetLastError();
+}
+cudaError_t launch_residual(const Grid& g, const double* b, const double* kx, const uint8_t* mask,
+                            double* r, cudaStream_t st) {
+  k_residual<<<nblk(g.nn, 256, 148 * 16), 256, 0, st>>>(g, b, kx, mask, r);
+  return cudaGetLastError();
+}
+cudaError_t launch_restrict(const Grid& gf, const Grid& gc, const double* rf, const uint8_t* maskc,
+                            double* rc, cudaStream_t st) {
+  k_restrict<<<nblk(gc.nn, 256, 148 * 16), 256, 0, st>>>(gf, gc, rf, maskc, rc);
+  return cudaGetLastError();
+}
+cudaError_t launch_prolong_add(const Grid& gf, const Grid& gc, const double* xc,
+                               const uint8_t* maskf, double* xf, cudaStream_t st) {
+  k_prolong_add<<<nblk(gf.nn, 256, 148 * 16), 256, 0, st>>>(gf, gc, xc, maskf, xf);
+  return cudaGetLastError();
+}
+cudaError_t launch_coarsen_E(const Grid& gf, const Grid& gc, const double* Ef, double* Ec,
+                             cudaStream_t st) {
+  k_coarsen_E<<<nblk(gc.ne, 256, 148 * 16), 256, 0, st>>>(gf, gc, Ef, Ec);
+  return cudaGetLastError();
+}
+cudaError_t launch_axpy2(long long n, double a, const double* x, double* y, double b,
+                         const double* z, double* w, cudaStream_t st) {
+  k_axpy2<<<nblk(n, 256, 148 * 8), 256, 0, st>>>(n, a, x, y, b, z, w);
+  return cudaGetLastError();
+}
+cudaError_t launch_xpby(long long n, const double* x, double b, double* y, cudaStream_t st) {
+  k_xpby<<<nblk(n, 256, 148 * 8), 256, 0, st>>>(n, x, b, y);
+  return cudaGetLastError();
+}
+cudaError_t launch_dot3(long long n, const double* a, const double* b, const double* c,
+                        double* partials, int nblocks, cudaStream_t st) {
+  k_dot3<<<nblocks, 256, 0, st>>>(n, a, b, c, partials);
+  return cudaGetLastError();
+}
+
+}  // namespace tomo

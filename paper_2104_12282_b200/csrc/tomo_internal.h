@@ -162,5 +162,22 @@ cudaError_t launch_dinv_dense(const Grid& g, const double* dinv_pad, double* out
                               cudaStream_t st);
 cudaError_t launch_coarsen(const Grid& g, int nb, const double* z, double* zc, cudaStream_t st);
 cudaError_t launch_dfma(double* out, int blocks, int iters, cudaStream_t st);
+cudaError_t launch_set_tol(Scal* s, double tol, cudaStream_t st);
+// multigrid (mg.cu)
+cudaError_t launch_jacobi_smooth(const Grid& g, double omega, const double* b, const double* kx,
+                                 const double* dinv, const uint8_t* mask, double* x, cudaStream_t st);
+cudaError_t launch_residual(const Grid& g, const double* b, const double* kx, const uint8_t* mask,
+                            double* r, cudaStream_t st);
+cudaError_t launch_restrict(const Grid& gf, const Grid& gc, const double* rf, const uint8_t* maskc,
+                            double* rc, cudaStream_t st);
+cudaError_t launch_prolong_add(const Grid& gf, const Grid& gc, const double* xc,
+                               const uint8_t* maskf, double* xf, cudaStream_t st);
+cudaError_t launch_coarsen_E(const Grid& gf, const Grid& gc, const double* Ef, double* Ec,
+                             cudaStream_t st);
+cudaError_t launch_axpy2(long long n, double a, const double* x, double* y, double b,
+                         const double* z, double* w, cudaStream_t st);
+cudaError_t launch_xpby(long long n, const double* x, double b, double* y, cudaStream_t st);
+cudaError_t launch_dot3(long long n, const double* a, const double* b, const double* c,
+                        double* partials, int nblocks, cudaStream_t st);
 
 }  // namespace tomo

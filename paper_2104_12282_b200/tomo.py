@@ -96,6 +96,11 @@ _SIGS = [
     ("tomo_bench_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_double)]),
     ("tomo_create_coarse", C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int]),
     ("tomo_coarsen", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64]),
+    ("tomo_mg_workspace_bytes", C.c_size_t, [C.c_void_p, C.c_int]),
+    ("tomo_mg_bind", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]),
+    ("tomo_mg_params", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_double]),
+    ("tomo_solve_mg", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_double,
+                                C.c_int, C.POINTER(SolveInfo)]),
 ]
 EXPORTS = [s[0] for s in _SIGS]
 
@@ -318,6 +323,26 @@ class Tomo:
         self._check(self.lib.tomo_coarsen(self.h, _ptr(_f64(z, self.n_e, "z")), nb,
                                           _ptr(_f64(out, n_ec, "zc")), n_ec))
         return out
+
+    # ------------------------------------------------------------------ multigrid
+    def mg_setup(self, levels: int, nu: int = 2, omega: float = 0.6, coarse_iters: int = 200,
+                 coarse_tol: float = 1e-3):
+        nbytes = self.lib.tomo_mg_workspace_bytes(self.h, levels)
+        if not nbytes:
+            raise TomoError(-1, f"{levels} MG levels impossible on this grid")
+        self.mg_workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base = self.mg_workspace.data_ptr()
+        self._check(self.lib.tomo_mg_bind(self.h, levels, C.c_void_p(base + (-base) % 256), nbytes))
+        self._check(self.lib.tomo_mg_params(self.h, nu, omega, coarse_iters, coarse_tol))
+
+    def solve_mg(self, rho: torch.Tensor, u: torch.Tensor | None = None, tol: float = 1e-10,
+                 max_iters: int = 2000):
+        u = self.zeros_dof() if u is None else u
+        info = SolveInfo()
+        self._check(self.lib.tomo_solve_mg(self.h, _ptr(_f64(rho, self.n_e, "rho")), self.n_e,
+                                           _ptr(_f64(u, self.n_dof, "u")), self.n_dof, tol, max_iters,
+                                           C.byref(info)))
+        return u, info
 
     # ------------------------------------------------------------------ introspection
     def ke(self):

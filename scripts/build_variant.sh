@@ -8,7 +8,7 @@ TMP=$(mktemp -d)
 git -C "$ROOT" archive "$REV" paper_2104_12282_b200/csrc include | tar -x -C "$TMP"
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 \
   -Xcompiler -fPIC -shared -cudart static -I "$TMP/include" "$@" \
-  "$TMP/paper_2104_12282_b200/csrc/api.cu" "$TMP/paper_2104_12282_b200/csrc/kernels.cu" \
+  $(ls "$TMP"/paper_2104_12282_b200/csrc/*.cu) \
   -o "$ROOT/paper_2104_12282_b200/lib/$NAME.so"
 rm -rf "$TMP"
 echo "$ROOT/paper_2104_12282_b200/lib/$NAME.so"
