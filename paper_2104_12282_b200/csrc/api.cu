@@ -63,9 +63,9 @@ struct tomo_ctx {
   OpArgs op_apply_P{}, op_apply_Z{};
   bool mg_bound = false;
   int mg_nu = 2;              // pre- and post-smoothing sweeps
-  double mg_omega = 0.6;      // damped Jacobi
-  int mg_coarse_iters = 200;  // coarsest level: fused Jacobi-PCG, loose tolerance
-  double mg_coarse_tol = 1e-3;
+  double mg_omega = 0.3;      // damped Jacobi (0.45 diverges at cfg3's 1e9 contrast)
+  int mg_coarse_iters = 30;   // coarsest level: fused Jacobi-PCG, loose tolerance
+  double mg_coarse_tol = 1e-2;
   // profiling
   bool prof = false;
   double prof_a_ms = 0, prof_b_ms = 0;

@@ -325,8 +325,8 @@ class Tomo:
         return out
 
     # ------------------------------------------------------------------ multigrid
-    def mg_setup(self, levels: int, nu: int = 2, omega: float = 0.6, coarse_iters: int = 200,
-                 coarse_tol: float = 1e-3):
+    def mg_setup(self, levels: int, nu: int = 2, omega: float = 0.3, coarse_iters: int = 30,
+                 coarse_tol: float = 1e-2):
         nbytes = self.lib.tomo_mg_workspace_bytes(self.h, levels)
         if not nbytes:
             raise TomoError(-1, f"{levels} MG levels impossible on this grid")
