@@ -407,9 +407,11 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
   const int fmb = ty * MB_W + org.om + tx, fmo = fmb + MB_W;
   const int fe = ty * E_W + org.oe + tx;                 // element (tx, ty)
 
-  // previous plane: node values of rows b, o (for the lower face) and the output node's
+  // previous plane: the output node's
   // p, z (PCG) or raw u (APPLY), D^-1, fixed bits
-  double vb_p[3] = {0.0, 0.0, 0.0}, vo_p[3] = {0.0, 0.0, 0.0};
+  double Fcar[12];  // face of the previous plane (carried in registers)
+#pragma unroll
+  for (int i = 0; i < 12; ++i) Fcar[i] = 0.0;
   double pv[3] = {0.0, 0.0, 0.0}, pz[3] = {0.0, 0.0, 0.0}, pdi = 0.0;
   unsigned pm = 0;
 
@@ -498,17 +500,17 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
     // ---- element row ty between node rows b and o (lane 31's results are never read;
     // skipping out-of-domain rows of edge tiles measured slower: 79.8 vs 78.4 us)
     double cup[3] = {0.0, 0.0, 0.0};
-    if (it >= 1) {
-      double Fc[12], Fn[12];
+    double Fn[12];  // face of this plane (the next plane's lower face)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double bn = __shfl_down_sync(0xffffffffu, vb[c], 1);
-        const double on = __shfl_down_sync(0xffffffffu, vo[c], 1);
-        const double bnp = __shfl_down_sync(0xffffffffu, vb_p[c], 1);
-        const double onp = __shfl_down_sync(0xffffffffu, vo_p[c], 1);
-        face_from(vb[c], bn, vo[c], on, Fn, c);
-        face_from(vb_p[c], bnp, vo_p[c], onp, Fc, c);
-      }
+    for (int c = 0; c < 3; ++c) {
+      const double bn = __shfl_down_sync(0xffffffffu, vb[c], 1);
+      const double on = __shfl_down_sync(0xffffffffu, vo[c], 1);
+      face_from(vb[c], bn, vo[c], on, Fn, c);
+    }
+    if (it >= 1) {
+      double Fc[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) Fc[i] = Fcar[i];
       double Gb[12], Gt[12];
 #ifdef TOMO_EXP_NO_CORE  // timing experiment only: bypass the element core
 #pragma unroll
@@ -581,9 +583,9 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
       acc[4] += qdq;
     }
 #pragma unroll
+    for (int i = 0; i < 12; ++i) Fcar[i] = Fn[i];
+#pragma unroll
     for (int c = 0; c < 3; ++c) {
-      vb_p[c] = vb[c];
-      vo_p[c] = vo[c];
       pv[c] = vo[c];
       pz[c] = zo[c];
     }
