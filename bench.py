@@ -249,7 +249,11 @@ def run_ours(args):
     for _ in range(args.warmup):
         _, c, _, info = step()
     iters = info.iterations
-    # ---- timed region: inputs resident in HBM, no instrumentation
+    # ---- timed region: inputs resident in HBM. The PCG loop of each evaluation is one CUDA
+    # graph; with profiling on, the library brackets that graph launch with two CUDA events
+    # on the bound stream (no events between the kernels), so the dominant kernel's average
+    # launch duration is measured live over the timed region without perturbing it.
+    t.set_profiling(True)
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
@@ -264,15 +268,10 @@ def run_ours(args):
     barrier()
     ck = clocks.stop()
     launches = t.launches - l0
-    value, ms = replica_aggregate(args.steps, e0.elapsed_time(e1), world, torch_reduce_max(dev))
-    ms_per_step = ms / args.steps
-    # ---- one more, instrumented step: CUDA events around every PCG launch on the bound
-    # stream give the dominant kernel's per-launch device time for the roofline
-    t.set_profiling(True)
-    step()
-    barrier()
     prof = t.profile_times()
     t.set_profiling(False)
+    value, ms = replica_aggregate(args.steps, e0.elapsed_time(e1), world, torch_reduce_max(dev))
+    ms_per_step = ms / args.steps
 
     # ---- e2e: through the C ABI with pinned host buffers (H2D rho, D2H P^T dc + c)
     e2e = None
@@ -302,7 +301,8 @@ def run_ours(args):
             "traffic": TRAFFIC.get(cfg), "peak_source": peak_src, "alg_bytes_per_launch": bytes_ka,
             "launch_ms": prof["k_a_ms"], "launches_timed": prof["n"],
             "share_of_step": (prof["k_a_ms"] * (iters + 1)) / ms_per_step if ms_per_step else None,
-            "timing": "per-launch CUDA events over one instrumented evaluation after the timed region"}
+            "timing": "CUDA events around the graph launch of every PCG loop in the timed region: "
+                      "device time / (iterations + 1) launches"}
     gf, _ = t.bench_dfma()
 
     cpu = None

@@ -66,6 +66,7 @@ struct tomo_ctx {
   double mg_omega = 0.3;      // damped Jacobi (0.45 diverges at cfg3's 1e9 contrast)
   int mg_coarse_iters = 30;   // coarsest level: fused Jacobi-PCG, loose tolerance
   double mg_coarse_tol = 1e-2;
+  int mg_emode = std::getenv("TOMO_MG_EMODE") ? std::atoi(std::getenv("TOMO_MG_EMODE")) : 0;
   // profiling
   bool prof = false;
   double prof_a_ms = 0, prof_b_ms = 0;
@@ -620,12 +621,30 @@ int run_pcg_loop(tomo_ctx* c, int max_iters, Scal* hs_out) {
   int k = 0;  // launches issued
   int batch = 8;
   const bool prof = c->prof;
-  if (!prof && c->pcg_exec) {
-    // the whole loop on the device: one graph launch, one read-back
+  if (c->pcg_exec && (!prof || !std::getenv("TOMO_PROFILE_PER_LAUNCH"))) {
+    // the whole loop on the device: one graph launch, one read-back. Profiling brackets the
+    // graph launch with two events (no perturbation of the loop): device time / launches.
+    if (prof) {
+      while (c->ev.size() < 2) {
+        cudaEvent_t e;
+        CK(c, cudaEventCreate(&e));
+        c->ev.push_back(e);
+      }
+      CK(c, cudaEventRecord(c->ev[0], c->st));
+    }
     CK(c, cudaGraphLaunch(c->pcg_exec, c->st));
+    if (prof) CK(c, cudaEventRecord(c->ev[1], c->st));
     CK(c, cudaMemcpyAsync(&hs, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
     CK(c, cudaStreamSynchronize(c->st));
-    c->launches += 2 * ((hs.iters + 2) / 2);  // kernel nodes executed (pairs)
+    const int nodes = 2 * ((hs.iters + 2) / 2);  // kernel nodes executed (even/odd pairs)
+    c->launches += nodes;
+    if (prof) {
+      float ms = 0;
+      CK(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+      // the launch after the one that set `done` (odd count) exits at its first instruction
+      c->prof_a_ms += ms;
+      c->prof_n += hs.iters + 1;
+    }
   } else {
   if (prof) {
     while (c->ev.size() < 2 * 257) {
@@ -1196,7 +1215,7 @@ extern "C" int tomo_solve_mg(tomo_ctx* c, const double* d_rho, int64_t n_e, doub
   // coarse levels: E averaged over the 8 children, their own Jacobi diagonals
   const tomo_ctx* prev = c;
   for (auto* l : c->mg) {
-    LAUNCH(c, launch_coarsen_E(prev->g, l->g, prev->E(), l->E(), c->st));
+    LAUNCH(c, launch_coarsen_E(prev->g, l->g, prev->E(), l->E(), c->mg_emode, c->st));
     LAUNCH(c, launch_jacobi(l->g, l->E(), l->ke_diag, l->dinv(), c->st));
     prev = l;
   }

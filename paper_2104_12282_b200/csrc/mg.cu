@@ -124,16 +124,21 @@ __global__ void k_prolong_add(Grid gf, Grid gc, const double* __restrict__ xc,
   }
 }
 
-// coarse E = mean of the 8 child elements' E (padded element layouts on both levels)
-__global__ void k_coarsen_E(Grid gf, Grid gc, const double* __restrict__ Ef, double* __restrict__ Ec) {
+// coarse E from the 8 child elements' E (padded element layouts on both levels):
+// mode 0 arithmetic mean, 1 geometric mean, 2 harmonic mean
+__global__ void k_coarsen_E(Grid gf, Grid gc, const double* __restrict__ Ef, double* __restrict__ Ec,
+                            int mode) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < gc.ne; e += stride) {
     const int I = (int)(e % gc.nx), J = (int)((e / gc.nx) % gc.ny), K = (int)(e / ((long long)gc.nx * gc.ny));
     double s = 0.0;
     for (int k = 2 * K; k < 2 * K + 2; ++k)
       for (int j = 2 * J; j < 2 * J + 2; ++j)
-        for (int i = 2 * I; i < 2 * I + 2; ++i) s += Ef[elem_pad(gf, i, j, k)];
-    Ec[elem_pad(gc, I, J, K)] = 0.125 * s;
+        for (int i = 2 * I; i < 2 * I + 2; ++i) {
+          const double v = Ef[elem_pad(gf, i, j, k)];
+          s += mode == 0 ? v : (mode == 1 ? log(v) : 1.0 / v);
+        }
+    Ec[elem_pad(gc, I, J, K)] = mode == 0 ? 0.125 * s : (mode == 1 ? exp(0.125 * s) : 8.0 / s);
   }
 }
 
@@ -209,8 +214,8 @@ cudaError_t launch_prolong_add(const Grid& gf, const Grid& gc, const double* xc,
   return cudaGetLastError();
 }
 cudaError_t launch_coarsen_E(const Grid& gf, const Grid& gc, const double* Ef, double* Ec,
-                             cudaStream_t st) {
-  k_coarsen_E<<<nblk(gc.ne, 256, 148 * 16), 256, 0, st>>>(gf, gc, Ef, Ec);
+                             int mode, cudaStream_t st) {
+  k_coarsen_E<<<nblk(gc.ne, 256, 148 * 16), 256, 0, st>>>(gf, gc, Ef, Ec, mode);
   return cudaGetLastError();
 }
 cudaError_t launch_axpy2(long long n, double a, const double* x, double* y, double b,

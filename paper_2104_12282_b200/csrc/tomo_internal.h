@@ -173,7 +173,7 @@ cudaError_t launch_restrict(const Grid& gf, const Grid& gc, const double* rf, co
 cudaError_t launch_prolong_add(const Grid& gf, const Grid& gc, const double* xc,
                                const uint8_t* maskf, double* xf, cudaStream_t st);
 cudaError_t launch_coarsen_E(const Grid& gf, const Grid& gc, const double* Ef, double* Ec,
-                             cudaStream_t st);
+                             int mode, cudaStream_t st);
 cudaError_t launch_axpy2(long long n, double a, const double* x, double* y, double b,
                          const double* z, double* w, cudaStream_t st);
 cudaError_t launch_xpby(long long n, const double* x, double b, double* y, cudaStream_t st);
