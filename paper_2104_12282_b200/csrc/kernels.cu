@@ -71,6 +71,22 @@ constexpr unsigned BYTES_PCG = 8u * (3 * VB_W * NR + DB_W * NR + E_W * ER) + MB_
 constexpr unsigned BYTES_PCG = 8u * (3 * VB_W * NR + OWN_N + DB_W * NR + E_W * ER) + MB_W * NR;
 #endif
 constexpr unsigned BYTES_APPLY = 8u * (VB_W * NR + E_W * ER) + MB_W * NR;
+// APPLY stages hold only u, E and the mask (9.7 KB): more of them fit, and they are needed
+// because a stage carries too few bytes to cover DRAM latency with two
+constexpr int NS_A = OP_NS_APPLY;
+constexpr int EE_OFF_A = al16(VB_W * NR);
+constexpr int MK_OFF_A = EE_OFF_A + al16(E_W * ER);
+constexpr int STAGE_A = MK_OFF_A + al16((MB_W * NR + 7) / 8);
+
+// per-mode pipeline geometry
+template <int MODE> struct Lay {
+  static constexpr int ns = NS, stage = STAGE, ee = EE_OFF, mk = MK_OFF;
+  static constexpr unsigned bytes = BYTES_PCG;
+};
+template <> struct Lay<OP_APPLY> {
+  static constexpr int ns = NS_A, stage = STAGE_A, ee = EE_OFF_A, mk = MK_OFF_A;
+  static constexpr unsigned bytes = BYTES_APPLY;
+};
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -307,7 +323,8 @@ __device__ __forceinline__ TileOrigin tile_origin(int i0) {
 template <int MODE>
 __device__ __forceinline__ void issue_plane(const OpArgs& a, double* stg, uint64_t* bar,
                                             const TileOrigin& o, int i0, int j0, int kq) {
-  mbar_expect_tx(bar, MODE == OP_PCG ? BYTES_PCG : BYTES_APPLY);
+  using L = Lay<MODE>;
+  mbar_expect_tx(bar, L::bytes);
   tma_load_3d(stg + R_OFF, &a.tm_in, o.xv, j0 - 1, kq, bar);
   if (MODE == OP_PCG) {
     tma_load_3d(stg + QO_OFF, &a.tm_qold, o.xv, j0 - 1, kq, bar);
@@ -317,8 +334,8 @@ __device__ __forceinline__ void issue_plane(const OpArgs& a, double* stg, uint64
 #endif
     tma_load_3d(stg + DI_OFF, &a.tm_dinv, o.xd, j0 - 1, kq, bar);
   }
-  tma_load_3d(stg + MK_OFF, &a.tm_mask, o.xm, j0 - 1, kq, bar);
-  tma_load_3d(stg + EE_OFF, &a.tm_E, o.xe, j0 - 1, kq - 1, bar);  // element plane kq-1
+  tma_load_3d(stg + L::mk, &a.tm_mask, o.xm, j0 - 1, kq, bar);
+  tma_load_3d(stg + L::ee, &a.tm_E, o.xe, j0 - 1, kq - 1, bar);  // element plane kq-1
   // warm L2 with a plane further ahead: the shared-memory stages are few (smem-bound), so
   // the bytes in flight that cover DRAM latency live in L2 instead
   const int kp = kq + OP_PF;
@@ -335,7 +352,10 @@ __device__ __forceinline__ void issue_plane(const OpArgs& a, double* stg, uint64
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
+    k_op(const __grid_constant__ OpArgs a) {
+  using L = Lay<MODE>;
+  constexpr int NS = L::ns, STAGE = L::stage;
   extern __shared__ __align__(128) double smem[];
   double* stages = smem;                     // [NS][STAGE]
   double* CD = stages + NS * STAGE;          // [2][3][NT] bottom-face contributions (by parity)
@@ -406,6 +426,11 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
   const int fdb = ty * DB_W + org.od + tx, fdo = fdb + DB_W;
   const int fmb = ty * MB_W + org.om + tx, fmo = fmb + MB_W;
   const int fe = ty * E_W + org.oe + tx;                 // element (tx, ty)
+  // owned-segment commit (PCG): stage offsets of node row ty+1 from node i0, and the node
+  // (within the segment) of positions tx, tx+32, tx+64
+  const int fown = (ty + 1) * VB_W + org.ov + 3;
+  const int down = (ty + 1) * DB_W + org.od + 1;
+  const int nd3[3] = {tx / 3, (tx + 32) / 3, (tx + 64) / 3};
 
   // previous plane: the output node's
   // p, z (PCG) or raw u (APPLY), D^-1, fixed bits
@@ -415,6 +440,9 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
   double pv[3] = {0.0, 0.0, 0.0}, pz[3] = {0.0, 0.0, 0.0}, pdi = 0.0;
   unsigned pm = 0;
 
+#ifdef TOMO_UNROLL2
+#pragma unroll 2
+#endif
   for (int it = 0; it < nit; ++it, ++git) {
     const int s = git % NS;
     double* stg = stages + s * STAGE;
@@ -438,22 +466,23 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
     continue;
 #endif
     // ---- stage node rows b = ty and o = ty+1: p = D^-1 r + beta p_old with
-    //      r = r_old - alpha q_old (PCG), or masked u (APPLY)
-    const unsigned char* MKb = reinterpret_cast<const unsigned char*>(stg + MK_OFF);
-    const unsigned mb = MKb[fmb], mo = MKb[fmo];
+    //      r = r_old - alpha q_old (PCG), or masked u (APPLY). PCG needs no masking here:
+    //      r_{-1}, q_{-1}, p_{-1} and u are zero at fixed DOFs (tomo_create rejects loads on
+    //      fixed DOFs, u0 is packed with the mask) and every launch writes r, p, q = 0 there
+    //      (q is masked at the output), so the staged values are already zero.
+    const unsigned char* MKb = reinterpret_cast<const unsigned char*>(stg + L::mk);
+    const unsigned mo = MKb[fmo];
     double vb[3], vo[3], zo[3], dio = 0.0;
     if (MODE == OP_PCG) {
       const double dib = stg[DI_OFF + fdb];
       dio = stg[DI_OFF + fdo];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double rb = ((mb >> c) & 1u) ? 0.0
-                          : fma(-alpha_prev, stg[QO_OFF + fvb + c], stg[R_OFF + fvb + c]);
-        vb[c] = ((mb >> c) & 1u) ? 0.0 : fma(beta, stg[PO_OFF + fvb + c], dib * rb);
-        const double ro = ((mo >> c) & 1u) ? 0.0
-                          : fma(-alpha_prev, stg[QO_OFF + fvo + c], stg[R_OFF + fvo + c]);
+        const double rb = fma(-alpha_prev, stg[QO_OFF + fvb + c], stg[R_OFF + fvb + c]);
+        vb[c] = fma(beta, stg[PO_OFF + fvb + c], dib * rb);
+        const double ro = fma(-alpha_prev, stg[QO_OFF + fvo + c], stg[R_OFF + fvo + c]);
         zo[c] = dio * ro;
-        vo[c] = ((mo >> c) & 1u) ? 0.0 : fma(beta, stg[PO_OFF + fvo + c], zo[c]);
+        vo[c] = fma(beta, stg[PO_OFF + fvo + c], zo[c]);
       }
       // owned updates of node row o, coalesced: lane l handles doubles l, l+32, l+64 of the
       // 90-double owned segment (nodes i0..i0+29), recomputed from the stage
@@ -464,16 +493,14 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
         for (int q = 0; q < 3; ++q) {
           const int pos = tx + 32 * q;  // position in the owned segment
           if (pos < own_lim) {
-            const int nd = pos / 3, c = pos - 3 * nd;  // node 1 + nd of the tile row, comp c
-            const int f = (ty + 1) * VB_W + org.ov + 3 + pos;
-            const bool fx = (MKb[(ty + 1) * MB_W + org.om + 1 + nd] >> c) & 1u;
-            const double di = stg[DI_OFF + (ty + 1) * DB_W + org.od + 1 + nd];
+            const int f = fown + pos;
+            const double di = stg[DI_OFF + down + nd3[q]];
             const double po = stg[PO_OFF + f];
-            const double rn = fx ? 0.0 : fma(-alpha_prev, stg[QO_OFF + f], stg[R_OFF + f]);
+            const double rn = fma(-alpha_prev, stg[QO_OFF + f], stg[R_OFF + f]);
             const double z = di * rn;
 #ifndef TOMO_EXP_NO_COMMIT_STORE  // timing experiment only (scripts/build_variant.sh)
             a.rnew[grow + pos] = rn;
-            a.pnew[grow + pos] = fx ? 0.0 : fma(beta, po, z);
+            a.pnew[grow + pos] = fma(beta, po, z);
 #ifdef TOMO_U_LDG
             a.u[grow + pos] = fma(alpha_prev, po, u_pre[q]);
 #else
@@ -488,6 +515,7 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
         acc[2] += rr;
       }
     } else {
+      const unsigned mb = MKb[fmb];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         vb[c] = ((mb >> c) & 1u) ? 0.0 : stg[R_OFF + fvb + c];
@@ -495,7 +523,7 @@ __global__ void __launch_bounds__(NT, OP_MINB) k_op(const __grid_constant__ OpAr
         vo[c] = ((mo >> c) & 1u) ? 0.0 : zo[c];
       }
     }
-    const double Ecur = stg[EE_OFF + fe];  // lane 31: a column outside the tile (unused)
+    const double Ecur = stg[L::ee + fe];  // lane 31: a column outside the tile (unused)
 
     // ---- element row ty between node rows b and o (lane 31's results are never read;
     // skipping out-of-domain rows of edge tiles measured slower: 79.8 vs 78.4 us)
@@ -1005,8 +1033,9 @@ int op_tiles(const Grid& g) {
   return ((g.nnx + OX - 1) / OX) * ((g.nny + OY - 1) / OY);
 }
 
-size_t op_smem(int /*mode*/) {
-  return sizeof(double) * ((size_t)NS * STAGE + (6 + GSN) * NT + 168) + sizeof(uint64_t) * NS + 16;
+size_t op_smem(int mode) {
+  const size_t ns = mode == OP_PCG ? NS : NS_A, st = mode == OP_PCG ? STAGE : STAGE_A;
+  return sizeof(double) * (ns * st + (6 + GSN) * NT + 168) + sizeof(uint64_t) * ns + 16;
 }
 
 static void op_attr() {

@@ -89,6 +89,14 @@ constexpr int OP_OY = OP_BY - 1;    // output nodes per tile along y
 #define TOMO_OP_NS 2
 #endif
 constexpr int OP_NS = TOMO_OP_NS;   // TMA pipeline stages (node planes in flight)
+#ifndef TOMO_OP_MINB_APPLY
+#define TOMO_OP_MINB_APPLY 2
+#endif
+constexpr int OP_MINB_APPLY = TOMO_OP_MINB_APPLY;  // resident blocks per SM of the K_hat u kernel
+#ifndef TOMO_OP_NS_APPLY
+#define TOMO_OP_NS_APPLY 6
+#endif
+constexpr int OP_NS_APPLY = TOMO_OP_NS_APPLY;  // stages of the K_hat u kernel (smaller stages)
 #ifndef TOMO_OP_PF
 #define TOMO_OP_PF 0
 #endif
