@@ -44,8 +44,10 @@ struct tomo_ctx {
       off_mask, off_cnt, off_ld, off_ldp, off_lv, off_taps, off_tw, off_part, off_scal, off_oc,
       off_end;
   size_t n_part = 0;
-  int op_blocks = 1;
+  int op_blocks = 1;   // fused PCG kernel grid
   int op_zchunks = 0;
+  int ap_blocks = 1;   // K_hat u kernel grid (its own occupancy)
+  int ap_zchunks = 0;
   int nb_b = 1, nb_s = 1, nb_oc = 1;
   int64_t launches = 0;
   int sms = 148;
@@ -476,9 +478,11 @@ int build_op_args(tomo_ctx* c) {
   base.ntiles = op_tiles(g);
   base.zchunks = c->op_zchunks;
   c->op_apply_u = base;
+  c->op_apply_u.zchunks = c->ap_zchunks;
   c->op_apply_u.tm_in = tm_u;
   c->op_apply_u.out = c->q(0);
   c->op_apply_p0 = base;
+  c->op_apply_p0.zchunks = c->ap_zchunks;
   c->op_apply_p0.tm_in = tm_p[0];
   c->op_apply_p0.out = c->q(0);
   // launch k reads the "old" buffers (k & 1) ^ 1 and writes the "new" ones k & 1
@@ -528,6 +532,32 @@ int build_pcg_graph(tomo_ctx* c) {
 }
 }  // namespace
 
+namespace {
+// Operator grid for `occ` resident blocks per SM. Persistent balanced schedule: one block per
+// resident slot, each with an equal contiguous share of the (tile, node plane) work list.
+// Synchronised (tile, z-chunk) blocks instead when that fills >= 85% of the slots: every
+// block marches the same planes at the same time, so neighbouring tiles share halos through
+// L2 (cfg3: DRAM reads 227 -> 171 MB per PCG launch).
+void op_schedule(const Grid& g, int occ, int sms, int* blocks, int* zchunks) {
+  if (occ < 1) occ = 1;
+  const long long tiles = op_tiles(g), slots = (long long)occ * sms;
+  const long long units = tiles * g.nnz;
+  const char* mp = std::getenv("TOMO_MIN_PLANES");  // A/B knob; default 1 plane per block (small grids are latency-bound)
+  const long long minp = mp ? std::max(1, std::atoi(mp)) : 1;
+  *blocks = (int)std::max<long long>(1, std::min<long long>(slots, units / minp));
+  *zchunks = 0;
+  const int ch = (int)std::max<long long>(1, std::min<long long>(g.nnz, slots / tiles));
+  const char* sc = std::getenv("TOMO_SCHED");
+  const bool force_sync = sc && std::strcmp(sc, "sync") == 0;
+  const bool force_bal = sc && std::strcmp(sc, "balanced") == 0;
+  const bool fills = tiles * ch >= (slots * 85) / 100 || ch == g.nnz;
+  if (force_sync || (fills && !force_bal)) {
+    *zchunks = ch;
+    *blocks = (int)(tiles * ch);
+  }
+}
+}  // namespace
+
 extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   if (!c) return TOMO_EINVAL;
   if (!d_ws || (reinterpret_cast<uintptr_t>(d_ws) & 255)) return fail(c, TOMO_EINVAL, "workspace must be 256-B aligned");
@@ -556,30 +586,8 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
     CK(c, cudaMemcpyAsync(c->tw(), c->tap_w.data(), sizeof(double) * c->tap_w.size(), cudaMemcpyHostToDevice, c->st));
   }
   LAUNCH(c, launch_filter_sums(g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), c->cnt(), c->st));
-  // persistent operator grid: one block per resident slot, each with an equal share of
-  // the (tile, node plane) work list; at least ~6 planes per block on small grids
-  int occ = op_occupancy(OP_PCG);
-  if (occ < 1) occ = 1;
-  const long long units = (long long)op_tiles(g) * g.nnz;
-  const char* mp = std::getenv("TOMO_MIN_PLANES");  // A/B knob; default 1 plane per block (small grids are latency-bound)
-  const long long minp = mp ? std::max(1, std::atoi(mp)) : 1;
-  c->op_blocks = (int)std::max<long long>(1, std::min<long long>((long long)occ * c->sms, units / minp));
-  c->op_zchunks = 0;
-  // synchronised (tile, z-chunk) blocks: every block marches the same planes at the same
-  // time, so neighbouring tiles share halos through L2 (cfg3: DRAM reads 227 -> 171 MB per
-  // launch). Used when it fills >= 85% of the resident slots; else the balanced schedule.
-  {
-    const long long tiles = op_tiles(g), slots = (long long)occ * c->sms;
-    const int ch = (int)std::max<long long>(1, std::min<long long>(g.nnz, slots / tiles));
-    const char* sc = std::getenv("TOMO_SCHED");
-    const bool force_sync = sc && std::strcmp(sc, "sync") == 0;
-    const bool force_bal = sc && std::strcmp(sc, "balanced") == 0;
-    const bool fills = tiles * ch >= (slots * 85) / 100 || ch == g.nnz;
-    if (force_sync || (fills && !force_bal)) {
-      c->op_zchunks = ch;
-      c->op_blocks = (int)(tiles * ch);
-    }
-  }
+  op_schedule(g, op_occupancy(OP_PCG), c->sms, &c->op_blocks, &c->op_zchunks);
+  op_schedule(g, op_occupancy(OP_APPLY), c->sms, &c->ap_blocks, &c->ap_zchunks);
   c->nb_b = (int)std::min<long long>((g.ndof_pad / 2 + 255) / 256, (long long)c->sms * 4);
   c->nb_s = (int)std::min<long long>((g.ne + 255) / 256, (long long)c->sms * 8);
   c->nb_oc = std::min(oc_max_blocks(), (int)std::max<long long>(1, (g.ne + 255) / 256));
@@ -691,7 +699,7 @@ int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) 
   Scal hs{};
   LAUNCH(c, launch_scal_init(c->scal(), tol * c->fnorm, max_iters, c->st));
   // r_{-1} := r0 = f - K u0 in r[1]; q_{-1} = p_{-1} = 0
-  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->ap_blocks, c->st));
   LAUNCH(c, launch_resid(g, c->q(0), c->r(1), c->ldp(), c->lv(), nl, c->st));
   CK(c, cudaMemsetAsync(c->q(1), 0, vb, c->st));
   CK(c, cudaMemsetAsync(c->p(1), 0, vb, c->st));
@@ -701,7 +709,7 @@ int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) 
                 hs.status == TOMO_ENAN ? "NaN/Inf in PCG" : "PCG breakdown: p^T K p <= 0 (SPEC.md l.173)");
   }
   // true residual ||f - K u||
-  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->ap_blocks, c->st));
   LAUNCH(c, launch_resid(g, c->q(0), c->r(0), c->ldp(), c->lv(), nl, c->st));
   LAUNCH(c, launch_norm2(g, c->r(0), c->scal(), c->part(), c->nb_b, c->st));
   CK(c, cudaMemcpyAsync(&hs, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
@@ -726,7 +734,7 @@ extern "C" int tomo_apply(tomo_ctx* c, const double* d_rho, int64_t n_e, const d
   if (d_u == d_y) return fail(c, TOMO_EINVAL, "u and y must not alias");
   if (int rc = prepare_modulus(c, d_rho, false)) return rc;
   LAUNCH(c, launch_pack(c->g, d_u, c->p(0), nullptr, c->st));
-  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_p0, c->op_blocks, c->st));
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_p0, c->ap_blocks, c->st));
   LAUNCH(c, launch_unpack(c->g, c->q(0), d_y, c->st));
   return TOMO_OK;
 }
@@ -975,9 +983,9 @@ extern "C" int tomo_bench_apply(tomo_ctx* c, const double* d_rho, int reps, doub
   cudaEvent_t e0, e1;
   CK(c, cudaEventCreate(&e0));
   CK(c, cudaEventCreate(&e1));
-  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));  // warm-up
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->ap_blocks, c->st));  // warm-up
   CK(c, cudaEventRecord(e0, c->st));
-  for (int i = 0; i < reps; ++i) LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));
+  for (int i = 0; i < reps; ++i) LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->ap_blocks, c->st));
   CK(c, cudaEventRecord(e1, c->st));
   CK(c, cudaEventSynchronize(e1));
   float ms = 0;
@@ -1104,12 +1112,12 @@ int mg_vcycle(tomo_ctx* f, int l, const double* b, double* x) {
   CK(c, cudaMemsetAsync(x, 0, vb, c->st));
   CK(c, cudaMemsetAsync(c->q(0), 0, vb, c->st));
   for (int s = 0; s < f->mg_nu; ++s) {
-    if (s > 0) LAUNCH(c, launch_op(OP_APPLY, ax, c->op_blocks, c->st));
+    if (s > 0) LAUNCH(c, launch_op(OP_APPLY, ax, c->ap_blocks, c->st));
     LAUNCH(c, launch_jacobi_smooth(g, om, b, c->q(0), c->dinv(), c->dmask(), x, c->st));
   }
   // residual, restriction, coarse correction, prolongation
   tomo_ctx* n = f->mg[l];
-  LAUNCH(c, launch_op(OP_APPLY, ax, c->op_blocks, c->st));
+  LAUNCH(c, launch_op(OP_APPLY, ax, c->ap_blocks, c->st));
   LAUNCH(c, launch_residual(g, b, c->q(0), c->dmask(), c->r(1), c->st));
   const bool coarsest_next = (l + 1 == L - 1);
   double* bn = coarsest_next ? n->r(1) : n->r(0);
@@ -1118,7 +1126,7 @@ int mg_vcycle(tomo_ctx* f, int l, const double* b, double* x) {
   LAUNCH(c, launch_prolong_add(g, n->g, n->u(), c->dmask(), x, c->st));
   // post-smoothing (same sweeps: symmetric cycle)
   for (int s = 0; s < f->mg_nu; ++s) {
-    LAUNCH(c, launch_op(OP_APPLY, ax, c->op_blocks, c->st));
+    LAUNCH(c, launch_op(OP_APPLY, ax, c->ap_blocks, c->st));
     LAUNCH(c, launch_jacobi_smooth(g, om, b, c->q(0), c->dinv(), c->dmask(), x, c->st));
   }
   return TOMO_OK;
@@ -1234,7 +1242,7 @@ extern "C" int tomo_solve_mg(tomo_ctx* c, const double* d_rho, int64_t n_e, doub
   int k = 0;
   bool conv = std::sqrt(rr) <= stop;
   while (!conv && k < max_iters) {
-    LAUNCH(c, launch_op(OP_APPLY, c->op_apply_P, c->op_blocks, c->st));  // Q = K P
+    LAUNCH(c, launch_op(OP_APPLY, c->op_apply_P, c->ap_blocks, c->st));  // Q = K P
     if (int rc = mg_dot3(c, Pv, Q, nullptr, d)) return rc;
     const double pq = d[0];
     if (!(pq > 0.0) || !std::isfinite(pq)) return fail(c, std::isnan(pq) ? TOMO_ENAN : TOMO_EBREAKDOWN, "MG-CG breakdown: p^T K p <= 0");
@@ -1253,7 +1261,7 @@ extern "C" int tomo_solve_mg(tomo_ctx* c, const double* d_rho, int64_t n_e, doub
   }
   // true residual, then u out
   CK(c, cudaMemcpyAsync(c->u(), U, vb, cudaMemcpyDeviceToDevice, c->st));
-  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->op_blocks, c->st));
+  LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->ap_blocks, c->st));
   LAUNCH(c, launch_resid(g, c->q(0), c->r(0), c->ldp(), c->lv(), (int)c->load_dofs.size(), c->st));
   LAUNCH(c, launch_norm2(g, c->r(0), c->scal(), c->part(), c->nb_b, c->st));
   LAUNCH(c, launch_unpack(g, U, d_u, c->st));

@@ -93,6 +93,18 @@ constexpr int OP_NS = TOMO_OP_NS;   // TMA pipeline stages (node planes in fligh
 #define TOMO_OP_MINB_APPLY 2
 #endif
 constexpr int OP_MINB_APPLY = TOMO_OP_MINB_APPLY;  // resident blocks per SM of the K_hat u kernel
+#ifndef TOMO_GSREG_APPLY
+#define TOMO_GSREG_APPLY 1
+#endif
+#ifndef TOMO_GSREG_PCG
+#define TOMO_GSREG_PCG 0
+#endif
+// carry the top face of the last element in registers (1) or shared memory (0)
+constexpr int OP_GSREG_APPLY = TOMO_GSREG_APPLY, OP_GSREG_PCG = TOMO_GSREG_PCG;
+#ifndef TOMO_PINGPONG_PCG
+#define TOMO_PINGPONG_PCG 0
+#endif
+constexpr bool OP_PINGPONG_PCG = TOMO_PINGPONG_PCG != 0;
 #ifndef TOMO_OP_NS_APPLY
 #define TOMO_OP_NS_APPLY 6
 #endif
