@@ -211,7 +211,7 @@ def run_reference(args):
 REF_ITERS = {"cfg3": 10488}
 # DRAM bytes per launch of the dominant kernel from one `ncu --set full` capture
 # (dram__bytes_read.sum + dram__bytes_write.sum), see profiles/.
-TRAFFIC = {"cfg3": 334932992}  # r1: 226.8 MB read + 108.1 MB written (profiles/r1_pcg_kernel_ncu.json)
+TRAFFIC = {"cfg3": 271643904}  # r1 session 3: 171.1 MB read + 100.5 MB written (profiles/r1s3_pcg_kernel_ncu.json)
 
 
 # ---------------------------------------------------------------- our arm
@@ -248,7 +248,6 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         _, c, _, info = step()
-    iters = info.iterations
     # ---- timed region: inputs resident in HBM. The PCG loop of each evaluation is one CUDA
     # graph; with profiling on, the library brackets that graph launch with two CUDA events
     # on the bound stream (no events between the kernels), so the dominant kernel's average
@@ -268,6 +267,7 @@ def run_ours(args):
     barrier()
     ck = clocks.stop()
     launches = t.launches - l0
+    iters = info.iterations
     prof = t.profile_times()
     t.set_profiling(False)
     value, ms = replica_aggregate(args.steps, e0.elapsed_time(e1), world, torch_reduce_max(dev))
@@ -304,6 +304,20 @@ def run_ours(args):
             "timing": "CUDA events around the graph launch of every PCG loop in the timed region: "
                       "device time / (iterations + 1) launches"}
     gf, _ = t.bench_dfma()
+    # ---- standalone K_hat u (BJ metric's second half): mean of 200 back-to-back launches of
+    # the operator kernel on the same rho, outside the timed region. Algorithmic bytes: read u,
+    # write y (8 B/DOF each), E (8 B/element), fixed mask (1 B/node); flops: the Walsh-basis
+    # element product, 213 per element
+    ap_ms = min(t.bench_apply(rho, reps=200) for _ in range(3))
+    ap_bytes = 16 * n_dof + 8 * n_e + n_n
+    ap_gbs = ap_bytes / (ap_ms * 1e-3) / 1e9
+    ap_gflops = 213 * n_e / (ap_ms * 1e-3) / 1e9
+    k_hat_u = {"kernel": "k_op<OP_APPLY>", "us": ap_ms * 1e3, "applications_per_s": 1e3 / ap_ms,
+               "dof_updates_per_s": n_dof * 1e3 / ap_ms, "alg_bytes": ap_bytes, "achieved_gbs": ap_gbs,
+               "hbm_frac": ap_gbs / hbm, "gflops": ap_gflops, "fp64_peak_gflops": gf,
+               "fp64_frac": ap_gflops / gf if gf else None,
+               "roofline_frac": max(ap_bytes / (hbm * 1e9), 213 * n_e / (gf * 1e9)) / (ap_ms * 1e-3)
+               if gf else None}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -324,7 +338,7 @@ def run_ours(args):
                            "x0": "zero (cold start)", "parallelism": f"replicas x{world}",
                            "l2": "PCG working set (6 vectors x 34.8 MB) exceeds the 126 MB L2"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": ck, "fp64_dfma_gflops_measured": gf}
+                "clocks": ck, "fp64_dfma_gflops_measured": gf, "k_hat_u": k_hat_u}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
