@@ -21,6 +21,10 @@ definitions in the paper's order:
                                                              (PAPER:176-180, 184; SPEC:217-238)
 * ``oc``     optimality-criteria update, canonical bisection
 * ``loop``   one exact-gradient evaluation and the SIMP loop (Eq. 2, 133-138 Alg. 1)
+* ``twoscale`` block averaging and BC restriction of the coarse path
+* ``mg``     Galerkin multigrid hierarchy and MG-preconditioned CG (SURVEY f2,
+             reading R5) - pinned by linear reproduction of P, the coarse rigid-body null
+             space and agreement with the direct solve
 
 Pins (tests/test_oracle_*.py, ``-m "not gpu"``): KE closed-form entries and
 spectrum, rigid-body null space, patch test, golden tiny compliances,

@@ -115,14 +115,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
       : "memory");
 }
 
-// L2 prefetch of a box (no shared memory, no completion tracking)
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int x, int y, int z) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
-                   reinterpret_cast<uint64_t>(tm)),
-               "r"(x), "r"(y), "r"(z)
-               : "memory");
-}
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -329,19 +321,6 @@ __device__ __forceinline__ void issue_plane(const OpArgs& a, double* stg, uint64
   }
   tma_load_3d(stg + L::mk, &a.tm_mask, o.xm, j0 - 1, kq, bar);
   tma_load_3d(stg + L::ee, &a.tm_E, o.xe, j0 - 1, kq - 1, bar);  // element plane kq-1
-  // warm L2 with a plane further ahead: the shared-memory stages are few (smem-bound), so
-  // the bytes in flight that cover DRAM latency live in L2 instead
-  const int kp = kq + OP_PF;
-  if (OP_PF > 0 && kp <= a.g.nz) {
-    tma_prefetch_3d(&a.tm_in, o.xv, j0 - 1, kp);
-    if (MODE == OP_PCG) {
-      tma_prefetch_3d(&a.tm_qold, o.xv, j0 - 1, kp);
-      tma_prefetch_3d(&a.tm_pold, o.xv, j0 - 1, kp);
-      tma_prefetch_3d(&a.tm_uown, 3 * i0, j0, kp);
-      tma_prefetch_3d(&a.tm_dinv, o.xd, j0 - 1, kp);
-    }
-    tma_prefetch_3d(&a.tm_E, o.xe, j0 - 1, kp - 1);
-  }
 }
 
 // per-thread state carried from one node plane to the next

@@ -109,13 +109,7 @@ constexpr bool OP_PINGPONG_PCG = TOMO_PINGPONG_PCG != 0;
 #define TOMO_OP_NS_APPLY 6
 #endif
 constexpr int OP_NS_APPLY = TOMO_OP_NS_APPLY;  // stages of the K_hat u kernel (smaller stages)
-#ifndef TOMO_OP_PF
-#define TOMO_OP_PF 0
-#endif
-// L2 prefetch distance (planes beyond the staged one); 0 = off. Measured at cfg3: off 79.8 us,
-// 2: 82.5, 3: 88.1, 4: 97.8, 6: 106.5 us per launch — extra TMA requests cost more than the
-// latency they hide, so it stays off.
-constexpr int OP_PF = TOMO_OP_PF;
+// (an L2 prefetch of planes 2-6 ahead measured slower at every distance: 82.5-106.5 vs 79.8 us)
 
 struct OpArgs {
   CUtensorMap tm_in;    // APPLY: u ; PCG: r_{k-1} (box 98 x (BY+1) doubles)
