@@ -31,7 +31,7 @@ for idx in range(5):
                "apply_ms": ms, "applies_per_s": 1e3 / ms, "dof_updates_per_s": p.n_dof * 1e3 / ms,
                "alg_bytes": b, "gbs": b / ms / 1e6, "hbm_frac": b / ms / 1e6 / hbm,
                "gflops": flops / ms / 1e6, "fp64_frac": flops / ms / 1e6 / gf}
-        if solve and p.n_elem <= 2_000_000:
+        if solve and p.n_elem <= 5_000_000:
             t.set_profiling(True)
             u, info = t.solve(rho, tol=1e-10, max_iters=50000)
             pt = t.profile_times()
