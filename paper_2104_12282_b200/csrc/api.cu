@@ -533,28 +533,34 @@ int build_pcg_graph(tomo_ctx* c) {
 }  // namespace
 
 namespace {
-// Operator grid for `occ` resident blocks per SM. Persistent balanced schedule: one block per
-// resident slot, each with an equal contiguous share of the (tile, node plane) work list.
-// Synchronised (tile, z-chunk) blocks instead when that fills >= 85% of the slots: every
-// block marches the same planes at the same time, so neighbouring tiles share halos through
-// L2 (cfg3: DRAM reads 227 -> 171 MB per PCG launch).
-void op_schedule(const Grid& g, int occ, int sms, int* blocks, int* zchunks) {
+// Operator grid for `occ` resident blocks per SM. Synchronised schedule: block = (tile,
+// z-chunk) with equal chunks, so the blocks of a wave march the same planes together and
+// neighbouring tiles share their halo rows through L2 (cfg3: DRAM reads 227 -> 171 MB per
+// PCG launch). The chunk count minimises waves x steps per block, waves = ceil(blocks /
+// resident slots), steps = planes per chunk + 2 (pipeline fill): cfg3 2 chunks (one wave),
+// 192x96x96 3 chunks, 256x128x128 5 chunks (three waves; measured 261 -> 191 us per PCG
+// launch against the persistent balanced schedule used before). The balanced schedule
+// (one block per slot, an equal contiguous share of the (tile, plane) list) remains for
+// grids with more tiles than the partials buffer holds blocks.
+void op_schedule(const Grid& g, int occ, int sms, int max_blocks, int* blocks, int* zchunks) {
   if (occ < 1) occ = 1;
   const long long tiles = op_tiles(g), slots = (long long)occ * sms;
   const long long units = tiles * g.nnz;
-  const char* mp = std::getenv("TOMO_MIN_PLANES");  // A/B knob; default 1 plane per block (small grids are latency-bound)
-  const long long minp = mp ? std::max(1, std::atoi(mp)) : 1;
-  *blocks = (int)std::max<long long>(1, std::min<long long>(slots, units / minp));
+  *blocks = (int)std::max<long long>(1, std::min<long long>(slots, units));
   *zchunks = 0;
-  const int ch = (int)std::max<long long>(1, std::min<long long>(g.nnz, slots / tiles));
-  const char* sc = std::getenv("TOMO_SCHED");
-  const bool force_sync = sc && std::strcmp(sc, "sync") == 0;
-  const bool force_bal = sc && std::strcmp(sc, "balanced") == 0;
-  const bool fills = tiles * ch >= (slots * 85) / 100 || ch == g.nnz;
-  if (force_sync || (fills && !force_bal)) {
-    *zchunks = ch;
-    *blocks = (int)(tiles * ch);
+  const char* sc = std::getenv("TOMO_SCHED");  // A/B knob: "balanced" | "sync"
+  if ((sc && std::strcmp(sc, "balanced") == 0) || tiles > max_blocks) return;
+  int ch = 1;
+  long long best = -1;
+  for (int c = 1; c <= g.nnz && tiles * c <= max_blocks; ++c) {
+    const long long waves = (tiles * c + slots - 1) / slots;
+    const long long cost = waves * ((g.nnz + c - 1) / c + 2);
+    if (best < 0 || cost < best) { best = cost; ch = c; }
   }
+  if (const char* zc = std::getenv("TOMO_ZCHUNKS"))  // A/B knob
+    ch = (int)std::max(1LL, std::min<long long>(std::min(g.nnz, std::atoi(zc)), max_blocks / tiles));
+  *zchunks = ch;
+  *blocks = (int)(tiles * ch);
 }
 }  // namespace
 
@@ -586,8 +592,8 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
     CK(c, cudaMemcpyAsync(c->tw(), c->tap_w.data(), sizeof(double) * c->tap_w.size(), cudaMemcpyHostToDevice, c->st));
   }
   LAUNCH(c, launch_filter_sums(g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), c->cnt(), c->st));
-  op_schedule(g, op_occupancy(OP_PCG), c->sms, &c->op_blocks, &c->op_zchunks);
-  op_schedule(g, op_occupancy(OP_APPLY), c->sms, &c->ap_blocks, &c->ap_zchunks);
+  op_schedule(g, op_occupancy(OP_PCG), c->sms, (int)(c->n_part / 5), &c->op_blocks, &c->op_zchunks);
+  op_schedule(g, op_occupancy(OP_APPLY), c->sms, (int)(c->n_part / 5), &c->ap_blocks, &c->ap_zchunks);
   c->nb_b = (int)std::min<long long>((g.ndof_pad / 2 + 255) / 256, (long long)c->sms * 4);
   c->nb_s = (int)std::min<long long>((g.ne + 255) / 256, (long long)c->sms * 8);
   c->nb_oc = std::min(oc_max_blocks(), (int)std::max<long long>(1, (g.ne + 255) / 256));
