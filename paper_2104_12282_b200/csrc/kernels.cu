@@ -32,13 +32,6 @@ namespace {
 constexpr int TX = 32;
 constexpr int BY = OP_BY;
 constexpr int NT = TX * BY;            // threads per operator block
-#ifndef TOMO_TMA_T
-#define TOMO_TMA_T 0
-#endif
-constexpr int OP_TMA_T = TOMO_TMA_T;   // the thread that issues the TMA loads
-#ifndef TOMO_COMMIT_PRED
-#define TOMO_COMMIT_PRED 0
-#endif
 constexpr int OX = OP_OX;              // output nodes per tile along x
 constexpr int OY = OP_OY;              // output nodes per tile along y
 constexpr int NS = OP_NS;              // pipeline stages
@@ -390,7 +383,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   const int i0 = (tile % tiles_x) * OX, j0 = (tile / tiles_x) * OY;
   const int nit = kend - kbeg + 2;
   const TileOrigin org = tile_origin(i0);
-  if (t == OP_TMA_T) {
+  if (t == 0) {
     for (int s = 0; s < NS && s < nit; ++s)
       issue_plane<MODE>(a, stages + ((git + s) % NS) * STAGE, &bars[(git + s) % NS], org, i0, j0,
                         kbeg - 1 + s);
@@ -459,23 +452,6 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           const int pos = tx + 32 * q;  // position in the owned segment
-#if TOMO_COMMIT_PRED
-          // loads always in the stage box (pos + 3 < VB_W); only the stores are predicated
-          const bool ok = pos < own_lim;
-          const int f = fown + pos;
-          const double di = stg[DI_OFF + down + nd3[q]];
-          const double po = stg[PO_OFF + f];
-          const double rn = ok ? fma(-alpha_prev, stg[QO_OFF + f], stg[R_OFF + f]) : 0.0;
-          const double z = di * rn;
-          const double pn = fma(beta, po, z), un = fma(alpha_prev, po, stg[UO_OFF + ty * OWN_W + pos]);
-          if (ok) {
-            a.rnew[grow + pos] = rn;
-            a.pnew[grow + pos] = pn;
-            a.u[grow + pos] = un;
-          }
-          rz = fma(z, rn, rz);
-          rr = fma(rn, rn, rr);
-#else
           if (pos < own_lim) {
             const int f = fown + pos;
             const double di = stg[DI_OFF + down + nd3[q]];
@@ -488,7 +464,6 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
             rz = fma(z, rn, rz);
             rr = fma(rn, rn, rr);
           }
-#endif
         }
         acc[1] += rz;
         acc[2] += rr;
@@ -540,7 +515,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
     }
     __syncthreads();  // CD of this plane complete; stage s consumed by every warp
     // (issuing from warp BY-1, which has no owned row, measured the same: 71.8 vs 71.4 us)
-    if (t == OP_TMA_T && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
+    if (t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
     // (a segment's last NS steps issue nothing, so the next segment starts with free stages)
 
     if (it >= 2 && mine) {
