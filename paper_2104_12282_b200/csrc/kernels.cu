@@ -508,10 +508,13 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
           const double m10 = (kGsReg ? P.G[3 + c] : GS[(3 + c) * NT + t]) + Gb[3 + c];
           const double m01 = (kGsReg ? P.G[6 + c] : GS[(6 + c) * NT + t]) + Gb[6 + c];
           const double m11 = (kGsReg ? P.G[9 + c] : GS[(9 + c) * NT + t]) + Gb[9 + c];
-          const double A_ = m00 - m01, B_ = m10 - m11, C_ = m00 + m01, D_ = m10 + m11;
-          const double y00 = A_ - B_, y10 = A_ + B_, y01 = C_ - D_, y11 = C_ + D_;
-          cup[c] = y01 + __shfl_up_sync(0xffffffffu, y11, 1);           // -> node row o (mine)
-          CDn[c * NT + t] = y00 + __shfl_up_sync(0xffffffffu, y10, 1);  // -> node row b
+          // inverse transform: the x butterfly first (corner x = 1 of element tx-1 comes from
+          // the lane below), then the y butterfly of the node column (8 DADD per component)
+          const double L0 = m00 - m10, L1 = m01 - m11, R0 = m00 + m10, R1 = m01 + m11;
+          const double c0 = L0 + __shfl_up_sync(0xffffffffu, R0, 1);
+          const double c1 = L1 + __shfl_up_sync(0xffffffffu, R1, 1);
+          cup[c] = c0 + c1;            // -> node row o (mine)
+          CDn[c * NT + t] = c0 - c1;   // -> node row b
         }
       }
 #pragma unroll
