@@ -537,7 +537,8 @@ namespace {
 // z-chunk) with equal chunks, so the blocks of a wave march the same planes together and
 // neighbouring tiles share their halo rows through L2 (cfg3: DRAM reads 227 -> 171 MB per
 // PCG launch). The chunk count minimises waves x steps per block, waves = ceil(blocks /
-// resident slots), steps = planes per chunk + 2 (pipeline fill): cfg3 2 chunks (one wave),
+// resident slots), steps = planes per chunk + 2 (pipeline fill; the first chunk skips the
+// warm-up on plane -1 and takes one plane more): cfg3 2 chunks (one wave),
 // 192x96x96 3 chunks, 256x128x128 5 chunks (three waves; measured 261 -> 191 us per PCG
 // launch against the persistent balanced schedule used before). The balanced schedule
 // (one block per slot, an equal contiguous share of the (tile, plane) list) remains for
@@ -554,7 +555,15 @@ void op_schedule(const Grid& g, int occ, int sms, int max_blocks, int* blocks, i
   long long best = -1;
   for (int c = 1; c <= g.nnz && tiles * c <= max_blocks; ++c) {
     const long long waves = (tiles * c + slots - 1) / slots;
-    const long long cost = waves * ((g.nnz + c - 1) / c + 2);
+    // steps of the longest chunk (the kernel's split: z_q = 1 + q (nnz - 1) / chunks, the
+    // first chunk skips the warm-up step on plane -1)
+    long long steps = 0;
+    auto zq = [&](int q) { return q == 0 ? 0 : std::min(g.nnz, 1 + (q * (g.nnz - 1)) / c); };
+    for (int q = 0; q < c; ++q) {
+      const int z0 = zq(q), z1 = zq(q + 1);
+      steps = std::max<long long>(steps, z1 - z0 + 2 - (q == 0 ? 1 : 0));
+    }
+    const long long cost = waves * steps;
     if (best < 0 || cost < best) { best = cost; ch = c; }
   }
   if (const char* zc = std::getenv("TOMO_ZCHUNKS"))  // A/B knob

@@ -359,8 +359,12 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
     // synchronised schedule: block = (tile, z-chunk), equal chunks, so every block marches
     // the same planes at the same time and neighbouring tiles share their halos through L2
     const int tile = blockIdx.x % a.ntiles, ch = blockIdx.x / a.ntiles;
-    ub = tile * g.nnz + (ch * g.nnz) / a.zchunks;
-    ue = tile * g.nnz + ((ch + 1) * g.nnz) / a.zchunks;
+    // chunk c = node planes [z_c, z_{c+1}), z_c = 1 + c (nnz - 1) / chunks: the first chunk
+    // gets one plane more because it skips the warm-up step on plane -1 (below), so every
+    // chunk costs the same number of steps (cfg3: 30 and 30 instead of 30 and 31)
+    auto zc = [&](int c) { return c == 0 ? 0 : min(g.nnz, 1 + (c * (g.nnz - 1)) / a.zchunks); };
+    ub = tile * g.nnz + zc(ch);
+    ue = tile * g.nnz + zc(ch + 1);
   } else {
     const long long units = (long long)a.ntiles * g.nnz;
     ub = (int)((units * blockIdx.x) / gridDim.x);
@@ -382,11 +386,14 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   u0 += kend - kbeg;
   const int i0 = (tile % tiles_x) * OX, j0 = (tile / tiles_x) * OY;
   const int nit = kend - kbeg + 2;
+  // step it stages node plane kbeg - 1 + it; plane -1 is all zeros (TMA out-of-bounds fill),
+  // and so is the state it would hand on, so a segment starting at plane 0 begins at step 1
+  const int it0 = kbeg == 0 ? 1 : 0;
   const TileOrigin org = tile_origin(i0);
   if (t == 0) {
-    for (int s = 0; s < NS && s < nit; ++s)
+    for (int s = 0; s < NS && it0 + s < nit; ++s)
       issue_plane<MODE>(a, stages + ((git + s) % NS) * STAGE, &bars[(git + s) % NS], org, i0, j0,
-                        kbeg - 1 + s);
+                        kbeg - 1 + it0 + s);
   }
 
   // output node (i0-1+tx, j0+ty) = top node of this warp's element row
@@ -552,7 +559,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   };
 
   if (MODE == OP_APPLY || OP_PINGPONG_PCG) {
-    int it = 0;
+    int it = it0;
     for (; it + 1 < nit; it += 2) {
       step(it, c0, c1);
       step(it + 1, c1, c0);
@@ -560,7 +567,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
     if (it < nit) step(it, c0, c1);
   } else {
     // (ping-pong measured slower for the fused PCG kernel: 76.9 vs 71.7 us at cfg3)
-    for (int it = 0; it < nit; ++it) {
+    for (int it = it0; it < nit; ++it) {
       step(it, c0, c1);
       c0 = c1;
     }
