@@ -195,8 +195,11 @@ class Tomo:
         self.n_e, self.n_n, self.n_dof, self.n_loads, self.n_taps = (int(v) for v in sz)
         nbytes = lib.tomo_workspace_bytes(h)
         with torch.cuda.device(self.device):
-            self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
             self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        # device buffers are allocated on the bound stream (the caching allocator then never
+        # hands them to another stream while the library may still use them)
+        with torch.cuda.stream(self.stream):
+            self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
         base = self.workspace.data_ptr()
         off = (-base) % 256
         self._check(lib.tomo_bind(h, C.c_void_p(base + off), nbytes, C.c_void_p(self.stream.cuda_stream)))
@@ -219,10 +222,13 @@ class Tomo:
             pass
 
     def zeros_dof(self):
-        return torch.zeros(self.n_dof, dtype=torch.float64, device=self.device)
+        # allocated and zeroed on the bound stream, where the library will read it
+        with torch.cuda.stream(self.stream):
+            return torch.zeros(self.n_dof, dtype=torch.float64, device=self.device)
 
     def zeros_elem(self):
-        return torch.zeros(self.n_e, dtype=torch.float64, device=self.device)
+        with torch.cuda.stream(self.stream):
+            return torch.zeros(self.n_e, dtype=torch.float64, device=self.device)
 
     @property
     def launches(self) -> int:
@@ -319,7 +325,8 @@ class Tomo:
 
     def coarsen(self, z: torch.Tensor, nb: int, out: torch.Tensor | None = None):
         n_ec = (self.p.nelx // nb) * (self.p.nely // nb) * (self.p.nelz // nb)
-        out = torch.zeros(n_ec, dtype=torch.float64, device=self.device) if out is None else out
+        with torch.cuda.stream(self.stream):
+            out = torch.zeros(n_ec, dtype=torch.float64, device=self.device) if out is None else out
         self._check(self.lib.tomo_coarsen(self.h, _ptr(_f64(z, self.n_e, "z")), nb,
                                           _ptr(_f64(out, n_ec, "zc")), n_ec))
         return out
@@ -330,7 +337,8 @@ class Tomo:
         nbytes = self.lib.tomo_mg_workspace_bytes(self.h, levels)
         if not nbytes:
             raise TomoError(-1, f"{levels} MG levels impossible on this grid")
-        self.mg_workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        with torch.cuda.stream(self.stream):
+            self.mg_workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
         base = self.mg_workspace.data_ptr()
         self._check(self.lib.tomo_mg_bind(self.h, levels, C.c_void_p(base + (-base) % 256), nbytes))
         self._check(self.lib.tomo_mg_params(self.h, nu, omega, coarse_iters, coarse_tol))
@@ -351,7 +359,8 @@ class Tomo:
         return torch.tensor(list(buf), dtype=torch.float64).reshape(24, 24)
 
     def fixed_mask(self):
-        m = torch.zeros(self.n_dof, dtype=torch.uint8, device=self.device)
+        with torch.cuda.stream(self.stream):
+            m = torch.zeros(self.n_dof, dtype=torch.uint8, device=self.device)
         self._check(self.lib.tomo_get_fixed_mask(self.h, _ptr(m)))
         return m
 
@@ -370,17 +379,20 @@ class Tomo:
         return [tuple(o[3 * i:3 * i + 3]) for i in range(n.value)], list(w)[: n.value]
 
     def element_dofs(self):
-        m = torch.empty(self.n_e * 24, dtype=torch.int64, device=self.device)
+        with torch.cuda.stream(self.stream):
+            m = torch.empty(self.n_e * 24, dtype=torch.int64, device=self.device)
         self._check(self.lib.tomo_get_element_dofs(self.h, _ptr(m)))
         return m.view(self.n_e, 24)
 
     def neighbor_counts(self):
-        m = torch.empty(self.n_e, dtype=torch.int32, device=self.device)
+        with torch.cuda.stream(self.stream):
+            m = torch.empty(self.n_e, dtype=torch.int32, device=self.device)
         self._check(self.lib.tomo_get_neighbor_counts(self.h, _ptr(m)))
         return m
 
     def jacobi(self, rho):
-        out = torch.empty(self.n_n, dtype=torch.float64, device=self.device)
+        with torch.cuda.stream(self.stream):
+            out = torch.empty(self.n_n, dtype=torch.float64, device=self.device)
         self._check(self.lib.tomo_get_jacobi(self.h, _ptr(_f64(rho, self.n_e, "rho")), _ptr(out)))
         return out
 
