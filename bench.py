@@ -260,9 +260,13 @@ def run_ours(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(st):
+        # per-step events on the same stream (one record between evaluations, ~800 ms apart)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         e0.record(st)
-        for _ in range(args.steps):
+        ev[0].record(st)
+        for i in range(args.steps):
             _, c, _, info = step()
+            ev[i + 1].record(st)
         e1.record(st)
     barrier()
     ck = clocks.stop()
@@ -271,6 +275,9 @@ def run_ours(args):
     prof = t.profile_times()
     t.set_profiling(False)
     value, ms = replica_aggregate(args.steps, e0.elapsed_time(e1), world, torch_reduce_max(dev))
+    step_ms = np.array([ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)])
+    step_dist = {"median": float(np.median(step_ms)), "p10": float(np.percentile(step_ms, 10)),
+                 "p90": float(np.percentile(step_ms, 90)), "n": int(args.steps), "rank": rank}
     ms_per_step = ms / args.steps
 
     # ---- e2e: through the C ABI with pinned host buffers (H2D rho, D2H P^T dc + c)
@@ -338,7 +345,8 @@ def run_ours(args):
                            "x0": "zero (cold start)", "parallelism": f"replicas x{world}",
                            "l2": "PCG working set (6 vectors x 34.8 MB) exceeds the 126 MB L2"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": ck, "fp64_dfma_gflops_measured": gf, "k_hat_u": k_hat_u}
+                "clocks": ck, "fp64_dfma_gflops_measured": gf, "k_hat_u": k_hat_u,
+                "step_ms_distribution": step_dist}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
