@@ -42,6 +42,43 @@ def aggregates(dims, a=3):
     return agg.ravel(), (gx, gy, gz)
 
 
+def strength_aggregates(A, bs, theta=0.08):
+    """Greedy standard aggregation on the node graph of strong connections: i-j strong if
+    ||A_ij||_F >= theta sqrt(||A_ii||_F ||A_jj||_F) (block norms). Phase 1: every node whose
+    strong neighbourhood is free seeds an aggregate of it; phase 2: leftovers join the
+    aggregate of a strong neighbour; phase 3: the rest form aggregates of themselves."""
+    A = sp.csr_matrix(A)
+    n = A.shape[0] // bs
+    Ab = sp.bsr_matrix(A, blocksize=(bs, bs))
+    Ab.sort_indices()
+    norms = np.sqrt((Ab.data ** 2).sum(axis=(1, 2)))
+    rows = np.repeat(np.arange(n), np.diff(Ab.indptr))
+    cols = Ab.indices
+    diag = np.zeros(n)
+    dm = rows == cols
+    diag[rows[dm]] = norms[dm]
+    strong = (norms >= theta * np.sqrt(diag[rows] * diag[cols])) & ~dm
+    S = sp.csr_matrix((np.ones(strong.sum()), (rows[strong], cols[strong])), shape=(n, n))
+    indptr, ind = S.indptr, S.indices
+    agg = -np.ones(n, dtype=np.int64)
+    na = 0
+    for i in range(n):  # phase 1
+        nb = ind[indptr[i]:indptr[i + 1]]
+        if agg[i] < 0 and (agg[nb] < 0).all():
+            agg[i] = na
+            agg[nb] = na
+            na += 1
+    for i in np.nonzero(agg < 0)[0]:  # phase 2
+        nb = ind[indptr[i]:indptr[i + 1]]
+        got = agg[nb][agg[nb] >= 0]
+        if got.size:
+            agg[i] = got[0]
+    for i in np.nonzero(agg < 0)[0]:  # phase 3
+        agg[i] = na
+        na += 1
+    return agg, na
+
+
 def tentative(B, agg, nagg, bs):
     """Block-diagonal P_tent with orthonormal columns spanning B on every aggregate; returns
     (P_tent, B_coarse) with B = P_tent B_coarse (bs DOFs per fine node, 6 near-null vectors)."""
@@ -53,7 +90,14 @@ def tentative(B, agg, nagg, bs):
     bounds = np.searchsorted(dof_agg[order], np.arange(nagg + 1))
     for g in range(nagg):
         idx = order[bounds[g]:bounds[g + 1]]
-        Q, R = np.linalg.qr(B[idx])
+        # rank-revealing factorisation B_agg = Q R (aggregates with fewer than 6 DOFs or
+        # with fixed nodes have rank < 6: the missing columns of Q are zero)
+        U, sv, Vt = np.linalg.svd(B[idx], full_matrices=False)
+        r = int((sv > 1e-12 * max(sv.max(), 1e-300)).sum()) if sv.size else 0
+        Q = np.zeros((len(idx), 6))
+        R = np.zeros((6, 6))
+        Q[:, :r] = U[:, :r]
+        R[:r] = sv[:r, None] * Vt[:r]
         rows.append(np.repeat(idx, 6)); cols.append(np.tile(6 * g + np.arange(6), len(idx)))
         vals.append(Q.ravel())
         Bc[6 * g:6 * g + 6] = R
@@ -86,7 +130,7 @@ def spectral_radius(A, Dinv, bs, its=30):
     return lam
 
 
-def hierarchy(A, fixed, n3, max_coarse=600):
+def hierarchy(A, fixed, n3, max_coarse=600, strength=False):
     levels = []
     B = rigid_modes(n3)
     B[fixed] = 0.0
@@ -95,10 +139,17 @@ def hierarchy(A, fixed, n3, max_coarse=600):
     while True:
         Dinv = block_dinv(A, bs)
         levels.append({"A": A, "Dinv": Dinv, "bs": bs})
-        if A.shape[0] <= max_coarse or max(dims) <= 2:
+        if A.shape[0] <= max_coarse or (not strength and max(dims) <= 2):
             break
-        agg, cdims = aggregates(dims)
-        nagg = int(np.prod(cdims))
+        if strength:
+            agg, nagg = strength_aggregates(A, bs, theta=0.08 if bs == 3 else 0.0)
+            cdims = (nagg, 1, 1)
+            print(f"  level {len(levels) - 1}: {A.shape[0] // bs} nodes -> {nagg} aggregates", flush=True)
+            if nagg > 0.5 * (A.shape[0] // bs):  # aggregation stalled: stop coarsening here
+                break
+        else:
+            agg, cdims = aggregates(dims)
+            nagg = int(np.prod(cdims))
         Pt, Bc = tentative(B, agg, nagg, bs)
         rho = spectral_radius(A, Dinv, bs)
         S = sp.csr_matrix(A)
@@ -158,15 +209,17 @@ def pcg(levels, f, tol=1e-10, max_iters=3000, nu=2, omega=0.6):
 
 
 if __name__ == "__main__":
-    s = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    s = int(sys.argv[1]) if len(sys.argv) > 1 else 4  # [--strength]
     p = dataclasses.replace(inputs.CONFIGS["cfg3"], nx=224 // s, ny=112 // s, nz=56 // s)
     rho = inputs.density_blobs_beta(p, sigma=6.0 / s)
     op = OracleProblem(p)
     A = op.Khat(rho)
     t0 = time.time()
-    levels = hierarchy(A, op.fixed, (p.nx, p.ny, p.nz))
+    strength = "--strength" in sys.argv
+    levels = hierarchy(A, op.fixed, (p.nx, p.ny, p.nz), strength=strength)
     print("levels", [L["A"].shape[0] for L in levels], f"setup {time.time() - t0:.1f}s", flush=True)
     for nu, om in [(2, 0.6), (2, 0.4)]:
         t0 = time.time()
         u, k = pcg(levels, op.f, nu=nu, omega=om)
-        print(f"cfg3/{s} SA-AMG nu={nu} omega={om}: {k} iterations, {time.time() - t0:.1f}s", flush=True)
+        tag = "strength" if strength else "structured"
+        print(f"cfg3/{s} SA-AMG ({tag}) nu={nu} omega={om}: {k} iterations, {time.time() - t0:.1f}s", flush=True)
