@@ -3,6 +3,7 @@
   python scripts/make_golden.py cfg1   # 50-iteration SIMP/OC loop history (BASELINE configs[1])
   python scripts/make_golden.py cfg2   # tight oracle solve of the MBB half-beam (configs[2])
   python scripts/make_golden.py cfg0   # tight oracle solve of configs[0]
+  python scripts/make_golden.py cfg3   # tight oracle solve of configs[3], sampled (about an hour)
 
 The oracle solves with its own Jacobi-PCG to a relative residual of 1e-12 (reading A14:
 tighter than the 1e-10 the parity runs use), from x0 = 0.
@@ -61,6 +62,40 @@ def tight(name):
     print(name, "done", meta)
 
 
+def cfg3_sampled(n_sample=4096, seed=33):
+    """configs[3] (4.35M DOFs): the oracle's own Jacobi-PCG to 1e-12 from x0 = 0 (about an
+    hour on 8-16 host cores), stored as c, the iteration count, the true residual, the
+    full-vector norms and seeded samples of u, dc and P^T dc ('full u parity
+    is run locally')."""
+    p = inputs.CFG3
+    rho = inputs.density_for("cfg3")
+    op = OracleProblem(p, assemble=False)
+    t = time.time()
+    u, its, conv, rel = op.solve_pcg(rho, tol=1e-12, max_iters=200000, use_csr=False)
+    r = op.f - op.apply(rho, u)
+    rel_true = float(np.linalg.norm(r) / np.linalg.norm(op.f))
+    c, dc, ce, dcf = op.evaluate(rho, u)
+    rng = np.random.default_rng(seed)
+    idof = np.sort(rng.choice(op.n_dof, n_sample, replace=False))
+    iel = np.sort(rng.choice(op.n_e, n_sample, replace=False))
+    meta = {"citation": "oracle Jacobi-PCG (tol 1e-12 recursive, x0 = 0, matrix-free apply) on BASELINE.json "
+                        "configs[3]; c = f^T u (Eq. 4), dc (Eq. 5, reading A5), dcf = P^T dc; seeded samples. "
+                        "Written by scripts/make_golden.py cfg3.",
+            "c": float(c), "pcg_iters_1e-12": int(its), "converged": bool(conv), "rel_res_recursive": float(rel),
+            "rel_res_true": rel_true, "norm_u": float(np.linalg.norm(u)), "norm_dc": float(np.linalg.norm(dc)),
+            "norm_dcf": float(np.linalg.norm(dcf)), "seconds": time.time() - t,
+            "dof_idx": idof.tolist(), "u": u[idof].tolist(), "elem_idx": iel.tolist(),
+            "dc": dc[iel].tolist(), "dcf": dcf[iel].tolist()}
+    with open(os.path.join(GOLD, "cfg3_sampled.json"), "w") as f:
+        json.dump(meta, f)
+    print("cfg3 done", {k: meta[k] for k in ("c", "pcg_iters_1e-12", "rel_res_true", "seconds")})
+
+
 if __name__ == "__main__":
     for a in sys.argv[1:]:
-        cfg1() if a == "cfg1" else tight(a)
+        if a == "cfg1":
+            cfg1()
+        elif a == "cfg3":
+            cfg3_sampled()
+        else:
+            tight(a)
