@@ -211,7 +211,7 @@ def run_reference(args):
 REF_ITERS = {"cfg3": 10488}
 # DRAM bytes per launch of the dominant kernel from one `ncu --set full` capture
 # (dram__bytes_read.sum + dram__bytes_write.sum), see profiles/.
-TRAFFIC = {"cfg3": 271155456}  # r1 session 3: DRAM read + write per launch (profiles/r1s3_pcg_kernel_ncu.json)
+TRAFFIC = {"cfg3": 272035584}  # r1 session 3 (committed kernel): DRAM read + write per launch (profiles/r1s3_pcg_kernel_ncu.json)
 
 
 # ---------------------------------------------------------------- our arm
