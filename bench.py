@@ -220,10 +220,11 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    torch.cuda.set_device(local)  # before the process group: NCCL binds the rank to this GPU
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", rank=rank, world_size=world)
-    torch.cuda.set_device(local)
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     from paper_2104_12282_b200 import inputs, tomo
 
