@@ -15,7 +15,10 @@ from .tomo import Tomo
 
 class SimpLoop:
     def __init__(self, t: Tomo, volfrac: float, move: float = 0.2, eta: float = 0.5,
-                 tol: float = 1e-10, max_iters: int = 50000):
+                 tol: float = 1e-10, max_iters: int = 50000, warm_start: bool = False):
+        # warm_start: each solve starts from the previous iteration's u instead of x0 = 0
+        # (reading A12 fixes x0 = 0 for parity runs, so the default is a cold start)
+        self.warm_start = warm_start
         self.t = t
         self.volfrac, self.move, self.eta = volfrac, move, eta
         self.tol, self.max_iters = tol, max_iters
@@ -29,7 +32,8 @@ class SimpLoop:
     def step(self, x: torch.Tensor):
         """One iteration from x_k: returns (x_{k+1}, c_k, lambda_k, oc_steps, pcg_info)."""
         self.t.filter(x, out=self.rho)
-        self.u.zero_()
+        if not self.warm_start:
+            self.u.zero_()
         _, c, _, info = self.t.evaluate(self.rho, self.u, self.dc, self.g, tol=self.tol,
                                          max_iters=self.max_iters)
         xn, lam, steps = self.t.oc_update(x, self.g, self.dv, self.volfrac, self.move, self.eta,

@@ -1,6 +1,6 @@
 """configs[3] 20-iteration SIMP/OC loop on the GPU: per-iteration PCG count,
 compliance, Lagrange multiplier and wall time (every step through the C ABI).
-    python scripts/time_loop_cfg3.py [out.json]"""
+    python scripts/time_loop_cfg3.py [out.json] [--warm]"""
 import json
 import os
 import sys
@@ -14,7 +14,8 @@ from paper_2104_12282_b200.loop import SimpLoop  # noqa: E402
 
 p = inputs.CFG3
 t = tomo.Tomo(tomo.params_from_problem(p), device="cuda:0")
-loop = SimpLoop(t, volfrac=p.volfrac, move=p.move, eta=p.eta, tol=1e-10)
+warm = "--warm" in sys.argv
+loop = SimpLoop(t, volfrac=p.volfrac, move=p.move, eta=p.eta, tol=1e-10, warm_start=warm)
 x = torch.tensor(inputs.density_for("cfg3"), dtype=torch.float64, device="cuda:0")
 rows = []
 t_all = time.perf_counter()
@@ -26,7 +27,8 @@ for k in range(p.loop_iters):
     rows.append({"k": k, "c": c, "lambda": lam, "oc_steps": steps, "pcg_iters": info.iterations,
                  "rel_res_true": info.rel_res_true, "seconds": time.perf_counter() - t0})
     print(json.dumps(rows[-1]), flush=True)
-out = {"config": p.name, "iterations": p.loop_iters, "seconds": time.perf_counter() - t_all, "rows": rows}
+out = {"config": p.name, "warm_start": warm, "iterations": p.loop_iters, "seconds": time.perf_counter() - t_all, "rows": rows}
 print(json.dumps({k: v for k, v in out.items() if k != "rows"}))
-if len(sys.argv) > 1:
-    json.dump(out, open(sys.argv[1], "w"), indent=1)
+outs = [a for a in sys.argv[1:] if not a.startswith("--")]
+if outs:
+    json.dump(out, open(outs[0], "w"), indent=1)
