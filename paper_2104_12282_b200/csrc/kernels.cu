@@ -465,9 +465,11 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
             const double po = stg[PO_OFF + f];
             const double rn = fma(-alpha_prev, stg[QO_OFF + f], stg[R_OFF + f]);
             const double z = di * rn;
+#ifndef TOMO_EXP_NO_COMMIT_STORE  // timing experiment only
             a.rnew[grow + pos] = rn;
             a.pnew[grow + pos] = fma(beta, po, z);
             a.u[grow + pos] = fma(alpha_prev, po, stg[UO_OFF + ty * OWN_W + pos]);
+#endif
             rz = fma(z, rn, rz);
             rr = fma(rn, rn, rr);
           }
@@ -506,7 +508,12 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
     double cup[3] = {0.0, 0.0, 0.0};
     if (it >= 1) {
       double Gb[12], Gt[12];
+#ifdef TOMO_EXP_NO_CORE  // timing experiment only: bypass the element core
+#pragma unroll
+      for (int i = 0; i < 12; ++i) { Gb[i] = P.F[i] * Ecur; Gt[i] = N.F[i] * Ecur; }
+#else
       element_core(P.F, N.F, Ecur, a.w, Gb, Gt);
+#endif
       if (it >= 2) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -544,7 +551,9 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
         const bool fixed = (P.pm >> c) & 1u;
         if (MODE == OP_PCG) {
           qv = fixed ? 0.0 : qv;
+#ifndef TOMO_EXP_NO_Q_STORE  // timing experiment only
           a.out[gb + c] = qv;
+#endif
           pq = fma(P.pv[c], qv, pq);
           zq = fma(P.pz[c], qv, zq);
           qdq = fma(P.pdi * qv, qv, qdq);
