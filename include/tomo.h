@@ -86,7 +86,10 @@ typedef struct {
 
 typedef struct {
   int iterations;           /* number of K_hat p products in the PCG loop (reading A11)   */
-  int converged;            /* 1 if ||r_k|| <= tol ||f|| (recursive residual)             */
+  int converged;            /* 1: ||r_k|| <= tol ||f|| (recursive) and the true residual
+                               ||f - K_hat u|| <= tol ||f||; 2: the recursive residual met
+                               tol but the true one did not (fp64 floor at high contrast);
+                               0: max_iters reached (not an error)          */
   double rel_res_recursive; /* ||r_k|| / ||f||                                            */
   double rel_res_true;      /* ||f - K_hat u|| / ||f|| recomputed at exit                 */
 } tomo_solve_info;
@@ -218,6 +221,10 @@ int64_t tomo_launch_count(const tomo_ctx* ctx);
  * sustained FP64 FMA rate (GFLOP/s, FMA = 2 flop) and the per-launch mean time of the
  * PCG kernels of the last tomo_solve measured with CUDA events on the bound stream.      */
 int tomo_bench_dfma(tomo_ctx* ctx, double* gflops_out, double* ms_out);
+/* PCG loop execution (default 1): 1 = the whole loop as one CUDA graph with a conditional
+ * WHILE node (one launch and one read-back per solve); 0 = host-batched launches of the
+ * same kernel (what ncu can profile: kernels inside conditional graphs are not captured). */
+int tomo_set_graph(tomo_ctx* ctx, int on);
 /* times[0] = mean ms per fused PCG launch, times[1] = 0 (no separate K_B kernel), times[2]
  * = number of launches timed. Requires tomo_set_profiling(ctx, 1) before the solve.      */
 int tomo_set_profiling(tomo_ctx* ctx, int on);

@@ -27,7 +27,10 @@ def x_new(x, g, dv, lam, move, eta):
 
 def oc_update(x, g, dv, P, volfrac, move=0.2, eta=0.5, l1=1e-30, l2=1e30, rel=1e-15,
               max_steps=200):
-    """Returns (x_new, lambda, steps, flips_trace) -- steps < 0 if the target was unreachable."""
+    """Returns (x_new, lambda, steps, flips_trace) -- steps < 0 if the target was unreachable.
+    Non-finite x, g or dv raise ValueError ("NaN in gradients -> error")."""
+    if not (np.all(np.isfinite(x)) and np.all(np.isfinite(g)) and np.all(np.isfinite(dv))):
+        raise ValueError("NaN/Inf in x, g or dv (SPEC:322)")
     target = volfrac * x.size
 
     def vol(xx):

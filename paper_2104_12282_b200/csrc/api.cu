@@ -3,8 +3,10 @@
 // Host-only work at tomo_create (KE by quadrature and its Walsh-basis core, BC mask and
 // load list, filter taps); device work is enqueued on the stream bound by tomo_bind into
 // the caller's workspace. tomo_bind also encodes the TMA tensor maps of the internal
-// (padded) PCG vectors. The PCG driver launches the fused K_A / K_B kernel pair per
-// iteration (kernels.cu) and reads the device scalars back once per batch of iterations.
+// (padded) PCG vectors. The PCG driver launches one fused single-pass PCG kernel per
+// iteration (kernels.cu, k_op<OP_PCG>), either as one CUDA graph with a conditional WHILE
+// node (default) or in host batches (tomo_set_graph(ctx, 0)), and reads the device
+// scalars back once per graph launch / batch.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -54,6 +56,7 @@ struct tomo_ctx {
   // operator launch variants (tensor maps bound to workspace buffers)
   OpArgs op_apply_u{}, op_apply_p0{}, op_pcg[2];  // op_pcg[k & 1] for launch k
   cudaGraph_t pcg_graph = nullptr;        // WHILE(not done) { launch even; launch odd }
+  bool use_graph = true;                  // tomo_set_graph: graph (1) or host batches (0)
   cudaGraphExec_t pcg_exec = nullptr;
   // multigrid hierarchy (tomo_mg_*): levels 1..L-1 are coarse contexts bound to the caller's
   // MG workspace; the outer flexible-CG vectors of the fine level live there too
@@ -190,7 +193,7 @@ bool walsh_coefficients(const double* KE, Walsh* W, double* maxdev) {
         if ((m >> d) & 1) s *= corner[a][d] ? 1.0 : -1.0;
       T[m][a] = s;
     }
-  static double D[24][24];
+  double D[24][24];  // local: tomo_create may run concurrently on several threads
   for (int m = 0; m < 8; ++m)
     for (int c = 0; c < 3; ++c)
       for (int n = 0; n < 8; ++n)
@@ -509,7 +512,7 @@ namespace {
 int build_pcg_graph(tomo_ctx* c) {
   if (c->pcg_exec) { cudaGraphExecDestroy(c->pcg_exec); c->pcg_exec = nullptr; }
   if (c->pcg_graph) { cudaGraphDestroy(c->pcg_graph); c->pcg_graph = nullptr; }
-  if (std::getenv("TOMO_NO_GRAPH")) return TOMO_OK;  // batched host loop (A/B timing)
+  if (!c->use_graph) return TOMO_OK;  // host-batched launches (tomo_set_graph(ctx, 0))
   CK(c, cudaGraphCreate(&c->pcg_graph, 0));
   cudaGraphConditionalHandle h;
   CK(c, cudaGraphConditionalHandleCreate(&h, c->pcg_graph, 1, cudaGraphCondAssignDefault));
@@ -580,6 +583,7 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   c->ws = static_cast<char*>(d_ws);
   c->ws_bytes = bytes;
   c->st = static_cast<cudaStream_t>(stream);
+  if (std::getenv("TOMO_NO_GRAPH")) c->use_graph = false;  // A/B knob, same as tomo_set_graph(ctx, 0)
   const Grid& g = c->g;
   int dev = 0;
   CK(c, cudaGetDevice(&dev));
@@ -731,7 +735,9 @@ int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) 
   CK(c, cudaStreamSynchronize(c->st));
   if (info) {
     info->iterations = hs.iters;
-    info->converged = hs.done == 1;
+    // 1: recursive AND true residual <= tol; 2: the recursive residual met tol but the true
+    // residual recomputed at exit did not (the fp64 floor of a high-contrast problem)
+    info->converged = hs.done != 1 ? 0 : (std::sqrt(hs.rr_true) <= tol * c->fnorm ? 1 : 2);
     info->rel_res_recursive = c->fnorm > 0 ? std::sqrt(hs.rr) / c->fnorm : 0.0;
     info->rel_res_true = c->fnorm > 0 ? std::sqrt(hs.rr_true) / c->fnorm : 0.0;
   }
@@ -831,11 +837,13 @@ extern "C" int tomo_oc_update(tomo_ctx* c, const double* d_x, const double* d_g,
     return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
   if (!(volfrac > 0 && volfrac <= 1) || !(move > 0) || !(eta > 0)) return fail(c, TOMO_EINVAL, "bad OC parameters");
   const double target = volfrac * (double)n_e;
+  CK(c, cudaMemsetAsync(c->ocout(), 0, sizeof(double) * 4, c->st));
   CK(c, launch_oc((int)n_e, d_x, d_g, d_dv, d_xnew, target, move, eta, c->part(), c->ocout(), c->nb_oc, c->st));
   ++c->launches;
-  double o[2];
+  double o[3];
   CK(c, cudaMemcpyAsync(o, c->ocout(), sizeof(o), cudaMemcpyDeviceToHost, c->st));
   CK(c, cudaStreamSynchronize(c->st));
+  if (o[2] != 0.0) return fail(c, TOMO_ENAN, "NaN/Inf in x, g or dv (SPEC.md l.322 \"NaN in gradients -> error\")");
   if (std::isnan(o[0])) return fail(c, TOMO_EBRACKET, "NaN in OC bisection (SPEC.md l.322)");
   if (lambda_out) *lambda_out = o[0];
   if (steps_out) *steps_out = (int)o[1];
@@ -972,6 +980,18 @@ extern "C" int tomo_bench_dfma(tomo_ctx* c, double* gflops_out, double* ms_out) 
   const double flops = 2.0 * 8 * 8 * (double)iters * 256.0 * blocks;
   if (gflops_out) *gflops_out = flops / (ms * 1e-3) / 1e9;
   if (ms_out) *ms_out = ms;
+  return TOMO_OK;
+}
+
+extern "C" int tomo_set_graph(tomo_ctx* c, int on) {
+  if (!c) return TOMO_EINVAL;
+  c->use_graph = on != 0;
+  if (!c->bound) return TOMO_OK;  // built at tomo_bind
+  if (c->use_graph && !c->pcg_exec) return build_pcg_graph(c);
+  if (!c->use_graph) {
+    if (c->pcg_exec) { cudaGraphExecDestroy(c->pcg_exec); c->pcg_exec = nullptr; }
+    if (c->pcg_graph) { cudaGraphDestroy(c->pcg_graph); c->pcg_graph = nullptr; }
+  }
   return TOMO_OK;
 }
 

@@ -1,9 +1,10 @@
 // libtomo kernels for sm_100a: the exact-gradient evaluation of arXiv 2104.12282.
 //
 //   k_op<OP_APPLY>  y = K_hat(rho) u
-//   k_op<OP_PCG>    fused PCG "K_A": p = D^-1 r + beta p_old, u += alpha p_old,
-//                   q = K_hat p, p^T q block partials -> alpha
-//   k_pcg_b         PCG "K_B": r -= alpha q, r^T r and r^T D^-1 r -> beta, convergence
+//   k_op<OP_PCG>    one single-pass Jacobi-PCG iteration: r = r_old - alpha q_old,
+//                   p = D^-1 r + beta p_old, u += alpha p_old, q = K_hat p, and the block
+//                   partials of p.q, r.z, r.r (+ the beta prediction terms); the last block
+//                   sets alpha, beta and the stop flag
 //   k_simp/k_jacobi SIMP modulus and Jacobi diagonal
 //   k_sens          Eq. 5 sensitivity
 //   k_filter        density filter P / P^T
@@ -13,14 +14,16 @@
 // values the 24x24 KE has 45 non-zeros. The operator takes the 2-D Walsh transform of every
 // node plane once per element column (shared by the two elements stacked on it), applies
 // the 7-coefficient core scaled by E_e, transforms back, and accumulates the top face of
-// one element with the bottom face of the next in registers. A 32 x 8 block owns a
-// 30 x 7 column of output nodes and marches along z through a chunk of node planes. Every
-// input plane tile (vector incl. halo, Jacobi, mask bytes, E, owned u) is fetched by ONE
-// thread with TMA (cp.async.bulk.tensor, OOB zero fill gives the domain boundary for free)
-// into a 3-stage mbarrier pipeline; outputs are written with coalesced stores.
+// one element with the bottom face of the next. A 32 x 8 block owns a 30 x 7 column of
+// output nodes and marches along z through a chunk of node planes. Every input plane tile
+// (vector incl. halo, Jacobi, mask bytes, E, owned u) is fetched by ONE thread with TMA
+// (cp.async.bulk.tensor, OOB zero fill gives the domain boundary for free) into an
+// OP_NS-stage (PCG) / OP_NS_APPLY-stage (K_hat u) mbarrier pipeline.
 // All reductions are two-stage and deterministic (fixed partition, fixed-order final sum
 // by the last block); there are no floating-point atomics.
 #include <cooperative_groups.h>
+
+#include <mutex>
 
 #include "tomo_internal.h"
 
@@ -888,6 +891,12 @@ __global__ void __launch_bounds__(256) k_oc(int ne, const double* __restrict__ x
   double l1 = 1e-30, l2 = 1e30;
   const double lo0 = l1, hi0 = l2;
   int steps = 0;
+  // SPEC.md l.322 "NaN in gradients -> error": flag non-finite x, g, dv (out2[2], zeroed by
+  // the host before the launch; every writer stores the same value)
+  bool bad = false;
+  for (long long e = g0; e < ne; e += stride)
+    bad |= !isfinite(x[e]) || !isfinite(gv[e]) || !isfinite(dv[e]);
+  if (bad) *(volatile double*)(out2 + 2) = 1.0;
   while (l2 > l1 * (1.0 + 1e-15) && steps < 200) {
     const double lm = sqrt(l1 * l2);
     double v = 0.0;
@@ -999,13 +1008,19 @@ size_t op_smem(int mode) {
   return sizeof(double) * (ns * st + (6 + GSN) * NT + 168) + sizeof(uint64_t) * ns + 16;
 }
 
+// The dynamic shared memory opt-in is a per-device function attribute: set it once per
+// device (several contexts may live on several GPUs of one process).
+static std::mutex g_attr_mu;
 static void op_attr() {
-  static bool done = false;
-  if (done) return;
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (dev < 0 || dev >= 64 || done[dev]) return;
   cudaFuncSetAttribute(k_op<OP_PCG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)op_smem(1));
   cudaFuncSetAttribute(k_op<OP_APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)op_smem(0));
-  done = true;
+  done[dev] = true;
 }
 
 cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st) {
@@ -1094,10 +1109,9 @@ cudaError_t launch_filter(const Grid& g, const int* taps, const double* w, int n
                           const double* Hs, const double* in, double* out, int transpose,
                           cudaStream_t st) {
   const size_t sm = (size_t)ntaps * (sizeof(double) + 3 * sizeof(int));
-  static size_t attr = 48 * 1024;
-  if (sm > attr) {
+  if (sm > 48 * 1024) {  // per device (as op_attr); cheap enough to set on every such launch
+    std::lock_guard<std::mutex> lk(g_attr_mu);
     cudaFuncSetAttribute(k_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = sm;
   }
   k_filter<<<nblk(g.ne, 256, 148 * 16), 256, sm, st>>>(g, taps, w, ntaps, Hs, in, out,
                                                        transpose);

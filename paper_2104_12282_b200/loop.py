@@ -33,7 +33,8 @@ class SimpLoop:
         """One iteration from x_k: returns (x_{k+1}, c_k, lambda_k, oc_steps, pcg_info)."""
         self.t.filter(x, out=self.rho)
         if not self.warm_start:
-            self.u.zero_()
+            with torch.cuda.stream(self.t.stream):  # the stream the library reads u on
+                self.u.zero_()
         _, c, _, info = self.t.evaluate(self.rho, self.u, self.dc, self.g, tol=self.tol,
                                          max_iters=self.max_iters)
         xn, lam, steps = self.t.oc_update(x, self.g, self.dv, self.volfrac, self.move, self.eta,

@@ -92,6 +92,7 @@ _SIGS = [
     ("tomo_launch_count", C.c_int64, [C.c_void_p]),
     ("tomo_bench_dfma", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("tomo_set_profiling", C.c_int, [C.c_void_p, C.c_int]),
+    ("tomo_set_graph", C.c_int, [C.c_void_p, C.c_int]),
     ("tomo_profile_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("tomo_bench_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_double)]),
     ("tomo_create_coarse", C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int]),
@@ -121,6 +122,23 @@ def load_library(path: str = LIB_PATH):
             fn.argtypes = args
         _lib = lib
     return _lib
+
+
+class _DeviceLib:
+    """libtomo calls made with this context's device current: the library launches on the
+    current device and reads its SM count from it (a context on cuda:1 must not run while
+    cuda:0 is current)."""
+
+    def __init__(self, lib, device: torch.device):
+        self._lib, self._dev = lib, device
+
+    def __getattr__(self, name):
+        fn = getattr(self._lib, name)
+
+        def call(*args):
+            with torch.cuda.device(self._dev):
+                return fn(*args)
+        return call
 
 
 def _ptr(t: torch.Tensor | None):
@@ -164,9 +182,11 @@ class Tomo:
         lib = load_library()
         if not torch.cuda.is_available():
             raise RuntimeError("libtomo needs a CUDA device (no CPU fallback)")
-        self.lib = lib
         self.p = p
         self.device = torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.lib = _DeviceLib(lib, self.device)
         if _handle is not None:  # context already created (tomo_create_coarse)
             self._bind(_handle, stream)
             return
@@ -177,6 +197,7 @@ class Tomo:
         bc = _BC(p.bc, p.load_total, fixed, len(p.fixed_dofs), ldofs, lvals, len(p.load_dofs))
         self._keep = (fixed, ldofs, lvals)
         h = C.c_void_p()
+        lib = self.lib
         rc = lib.tomo_create(C.byref(h), C.byref(g), p.E0, p.Emin, p.nu, p.penal, p.rmin, C.byref(bc))
         self.h = h
         if rc != 0:
@@ -402,6 +423,10 @@ class Tomo:
         ms = C.c_double()
         self._check(self.lib.tomo_bench_dfma(self.h, C.byref(gf), C.byref(ms)))
         return gf.value, ms.value
+
+    def set_graph(self, on: bool):
+        """PCG loop as one CUDA graph (default) or host-batched launches (ncu-visible)."""
+        self._check(self.lib.tomo_set_graph(self.h, 1 if on else 0))
 
     def set_profiling(self, on: bool):
         self._check(self.lib.tomo_set_profiling(self.h, 1 if on else 0))

@@ -1,4 +1,4 @@
-"""Exploration (not collected by pytest; lives under tests/ because it runs the oracle):
+"""Exploration of SURVEY f2 on the CPU oracle (not a test; calls only oracle/ and inputs):
 smoothed-aggregation multigrid with the six rigid-body modes as near-null space, as the
 preconditioner of CG, on the cfg3 density recipe at reduced size. Question answered: does a
 coarse space that contains the rigid motions of every aggregate (hence of every solid
@@ -9,7 +9,7 @@ Structured aggregation: 3x3x3 node blocks per level (the coarse "nodes" are the 
 on a structured grid, 6 DOFs each); tentative P = per-aggregate orthonormalised rigid modes;
 P = (I - omega D^-1 A) P_tent, omega = 4/3 / rho(D^-1 A); A_c = P^T A P; symmetric
 block-Jacobi (3x3 or 6x6 diagonal blocks) V-cycle; coarsest exact.
-    python tests/explore_sa_amg.py 4      # 1/4-size cfg3 recipe
+    python scripts/explore/explore_sa_amg.py 4      # 1/4-size cfg3 recipe
 """
 import dataclasses
 import sys
@@ -19,7 +19,7 @@ import numpy as np
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
-sys.path.insert(0, __file__.rsplit("/tests/", 1)[0])
+sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
 from oracle.loop import OracleProblem  # noqa: E402
 from paper_2104_12282_b200 import inputs  # noqa: E402
 

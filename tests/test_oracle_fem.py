@@ -71,6 +71,85 @@ def test_mbb_half_preset():
     assert not fixed[dofs].any()
 
 
+def _decode(dofs, nx, ny):
+    """DOF -> (i, j, k, c) by the numbering of SPEC:26/30 (x fastest)."""
+    out = []
+    for d in np.asarray(dofs).tolist():
+        n, c = divmod(d, 3)
+        i = n % (nx + 1)
+        j = (n // (nx + 1)) % (ny + 1)
+        k = n // ((nx + 1) * (ny + 1))
+        out.append((i, j, k, c))
+    return out
+
+
+@pytest.mark.parametrize("dims", [(5, 3, 4), (2, 1, 1), (7, 4, 2)])
+def test_cantilever_preset_locations(dims):
+    """Exact DOF sets of the cantilever preset, written from the text of BASELINE.json
+    configs[0] ("x=0 face fully clamped; total load -1 in z spread evenly over the nodes of
+    the bottom edge of the x=max face"; reading A8): fixed = every DOF of every node with
+    i = 0; loaded = the z DOF of the nodes (nx, j, 0), j = 0..ny, each -1/(ny+1)."""
+    nx, ny, nz = dims
+    fixed, dofs, vals = grid.cantilever_bc(nx, ny, nz, -1.0)
+    want_fixed = {(0, j, k, c) for j in range(ny + 1) for k in range(nz + 1) for c in range(3)}
+    assert set(_decode(np.flatnonzero(fixed), nx, ny)) == want_fixed
+    assert sorted(_decode(dofs, nx, ny)) == [(nx, j, 0, 2) for j in range(ny + 1)]
+    assert np.all(vals == -1.0 / (ny + 1))
+
+
+@pytest.mark.parametrize("dims", [(5, 3, 4), (4, 2, 2), (3, 1, 5)])
+def test_mbb_half_preset_locations(dims):
+    """Exact DOF sets of the MBB half-beam preset from BASELINE.json configs[2] ("symmetry
+    (u_x=0) on the x=0 face, roller (u_z=0) on the bottom edge line at x=max, unit -z line
+    load on the top edge at x=0") plus reading A9's u_y pin at node (nx, 0, 0) and A10's
+    equal weights: fixed = {(0,j,k,x)} U {(nx,j,0,z)} U {(nx,0,0,y)}; loaded = {(0,j,nz,z)}."""
+    nx, ny, nz = dims
+    fixed, dofs, vals = grid.mbb_half_bc(nx, ny, nz, -1.0)
+    want = {(0, j, k, 0) for j in range(ny + 1) for k in range(nz + 1)}
+    want |= {(nx, j, 0, 2) for j in range(ny + 1)}
+    want |= {(nx, 0, 0, 1)}
+    assert set(_decode(np.flatnonzero(fixed), nx, ny)) == want
+    assert sorted(_decode(dofs, nx, ny)) == [(0, j, nz, 2) for j in range(ny + 1)]
+    assert np.all(vals == -1.0 / (ny + 1))
+
+
+def test_mbb_half_equals_mirrored_full_beam():
+    """Physics pin of the MBB half-beam preset, independent of grid.mbb_half_bc: the full
+    simply supported beam of PAPER:207 ("MBB beam", load at the top centre), 2nx long,
+    rollers u_z = 0 on the bottom edge lines x' = 0 and x' = 2nx, line load -2 on the top
+    centre line x' = nx, rigid motions removed symmetrically (u_x at (nx,0,0), u_y at
+    (0,0,0) and (2nx,0,0)). By mirror symmetry its right half x' = nx + x is the half-beam
+    with u_x = 0 on the symmetry plane, the roller at x = nx, load -1 at x = 0 and the u_y
+    pin at (nx,0,0) - so u agrees node by node and c_full = 2 c_half. A load on the wrong
+    edge, a roller at x = 0 or the u_y pin at (0,0,0) all fail this."""
+    nx, ny, nz = 4, 2, 3
+    half = OracleProblem(inputs.Problem("half", nx, ny, nz, bc=inputs.BC_MBB_HALF))
+    rng = np.random.default_rng(7)
+    rho_half = rng.uniform(0.3, 1.0, half.n_e).reshape(nz, ny, nx)
+    u_half = half.solve_direct(rho_half.ravel())
+    # full beam: element (i', j, k) of the right half is the half's (i' - nx); left half mirrored
+    NX = 2 * nx
+    rho_full = np.concatenate([rho_half[:, :, ::-1], rho_half], axis=2).ravel()
+    _, _, n_dof = grid.counts(NX, ny, nz)
+    nid = lambda i, j, k: i + (NX + 1) * (j + (ny + 1) * k)  # noqa: E731
+    fixed = np.zeros(n_dof, dtype=bool)
+    for j in range(ny + 1):
+        fixed[3 * nid(0, j, 0) + 2] = fixed[3 * nid(NX, j, 0) + 2] = True
+    fixed[3 * nid(nx, 0, 0) + 0] = True
+    fixed[3 * nid(0, 0, 0) + 1] = fixed[3 * nid(NX, 0, 0) + 1] = True
+    f = np.zeros(n_dof)
+    for j in range(ny + 1):
+        f[3 * nid(nx, j, nz) + 2] = -2.0 / (ny + 1)
+    KE = fem.element_stiffness(0.3)
+    E = fem.simp(rho_full, 1.0, 1e-9, 3.0)
+    K = fem.apply_bc(fem.assemble(grid.element_dofs(NX, ny, nz), E, KE, n_dof), fixed)
+    u_full = solve.direct_solve(K, f)
+    assert math.isclose(f @ u_full, 2.0 * (half.f @ u_half), rel_tol=1e-10)
+    uf = u_full.reshape(nz + 1, ny + 1, NX + 1, 3)[:, :, nx:, :]
+    uh = u_half.reshape(nz + 1, ny + 1, nx + 1, 3)
+    assert np.max(np.abs(uf - uh)) <= 1e-9 * np.max(np.abs(uh))
+
+
 # ------------------------------------------------------------------ KE
 @pytest.mark.parametrize("nu", [0.3, 0.25, 0.45])
 def test_ke_closed_form(nu):
