@@ -8,9 +8,10 @@ dc (Eq. 5), filtered sensitivity P^T dc — all in libtomo's CUDA kernels throug
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg3]
 
-N > 1 (torchrun): replicas only — every rank evaluates its own copy of the
-problem; value = evaluations of all ranks / max-over-ranks time. The reference arm
-(--impl reference) is the CPU oracle timed on this box's host cores on a bounded sample.
+N > 1 (torchrun, or self-launched when WORLD_SIZE is unset): replicas only —
+every rank evaluates its own copy of the problem; value = evaluations of all ranks /
+max-over-ranks time. The reference arm (--impl reference) is the CPU oracle timed on this
+box's host cores on a bounded sample (>= 100 PCG iterations, phases timed separately).
 """
 from __future__ import annotations
 
@@ -41,6 +42,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tol", type=float, default=1e-10)
+    # CPU test of the multi-rank launch path: each rank sleeps instead of evaluating (no GPU)
+    ap.add_argument("--mock", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -132,83 +135,162 @@ def torch_reduce_max(device):
 
 
 # ---------------------------------------------------------------- CPU oracle baseline
-def oracle_sample(cfg: str, n_iters_full: int | None, budget_iters: int = 4):
-    """Time the oracle (as it stands) on a bounded sample of one evaluation of `cfg`:
-    setup + `budget_iters` PCG iterations + compliance/sensitivity/filter-transpose, then
-    project a full evaluation with the measured iteration count. Returns (evals/s, desc, cores)."""
-    from oracle.loop import OracleProblem  # test infrastructure, used only for this baseline leg
-    from oracle import fem, filt
-    from paper_2104_12282_b200 import inputs
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    p = inputs.CONFIGS[cfg]
-    rho = inputs.density_for(cfg)
-    t0 = time.perf_counter()
-    op = OracleProblem(p, assemble=False)
-    E = op.E(rho)
-    dinv = 1.0 / fem.jacobi_diag(E, op.KE, op.edof, op.fixed)
-    t_setup = time.perf_counter() - t0
-    # PCG iterations: one apply + vector updates each (oracle solve.pcg body)
-    u = np.zeros(op.n_dof)
-    r = op.f.copy()
-    z = dinv * r
-    pv = z.copy()
-    rz = r @ z
-    t0 = time.perf_counter()
-    for _ in range(budget_iters):
-        q = fem.apply_matfree(pv, E, op.KE, op.edof, op.fixed)
-        alpha = rz / (pv @ q)
-        u += alpha * pv
-        r -= alpha * q
-        _ = np.linalg.norm(r)
-        z = dinv * r
-        rzn = r @ z
-        pv = z + (rzn / rz) * pv
-        rz = rzn
-    t_iter = (time.perf_counter() - t0) / budget_iters
-    t0 = time.perf_counter()
-    _c, dc, _ce, dcf = op.evaluate(rho, u)
-    t_grad = time.perf_counter() - t0
-    n_it = n_iters_full if n_iters_full else budget_iters
-    t_eval = t_setup + n_it * t_iter + t_grad
-    cores = len(os.sched_getaffinity(0))
-    desc = (f"oracle (numpy/scipy, fp64) on {cfg}: setup {t_setup:.2f}s + {budget_iters} timed PCG "
-            f"iterations ({t_iter:.3f}s each) + gradient {t_grad:.2f}s, projected to {n_it} iterations "
-            f"(the GPU solve's count) = {t_eval:.1f}s per evaluation")
-    return 1.0 / t_eval, desc, cores
+
+def blas_threads() -> int | None:
+    try:
+        from threadpoolctl import threadpool_info
+        return max((d.get("num_threads", 1) for d in threadpool_info()), default=None)
+    except Exception:
+        return None
+
+
+def oracle_iters(cfg: str):
+    """The ORACLE's own Jacobi-PCG iteration count to 1e-10 from x0 = 0 on `cfg`, as recorded
+    by scripts/make_golden.py (a stored oracle result, not the CUDA path's count)."""
+    name = {"cfg3": "cfg3_sampled.json"}.get(cfg, f"{cfg}_solve.json")
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", name)) as f:
+            g = json.load(f)
+        return g.get("pcg_iters_1e-10")
+    except (OSError, ValueError):
+        return None
+
+
+class OracleSample:
+    """The CPU oracle as it stands (oracle/, test infrastructure; used here only for the
+    cpu_baseline / --impl reference legs), timed phase by phase on a bounded sample of one
+    exact-gradient evaluation of `cfg`: setup (element DOF map, KE, SIMP, Jacobi diagonal),
+    Jacobi-PCG iterations (oracle.solve.pcg with the matrix-free apply, from x0 = 0, tol 0 so
+    that exactly n iterations run), compliance, sensitivity, filter (build P + P^T dc).
+    A full evaluation is projected as setup + N_oracle x t_iter + gradient phases, N_oracle
+    being the oracle's own iteration count to 1e-10 (tests/golden, scripts/make_golden.py)."""
+
+    def __init__(self, cfg: str):
+        from oracle import fem
+        from oracle.loop import OracleProblem
+        from paper_2104_12282_b200 import inputs
+
+        self.cfg = cfg
+        self.p = inputs.CONFIGS[cfg]
+        self.rho = inputs.density_for(cfg)
+        t0 = time.perf_counter()
+        self.op = OracleProblem(self.p, assemble=False)
+        self.E = self.op.E(self.rho)
+        self.dinv = 1.0 / fem.jacobi_diag(self.E, self.op.KE, self.op.edof, self.op.fixed)
+        self.t_setup = time.perf_counter() - t0
+        self.iter_times = []  # seconds per iteration of each timed sample
+        self.n_timed = 0
+        self.u = None
+        self.phases = None
+
+    def _apply(self, v):
+        from oracle import fem
+        return fem.apply_matfree(v, self.E, self.op.KE, self.op.edof, self.op.fixed)
+
+    def iterate(self, n: int) -> float:
+        from oracle import solve
+        t0 = time.perf_counter()
+        u, k, _, _ = solve.pcg(self._apply, self.dinv, self.op.f, tol=0.0, max_iters=n)
+        dt = (time.perf_counter() - t0) / max(k, 1)
+        self.iter_times.append(dt)
+        self.n_timed += k
+        self.u = u
+        return dt
+
+    def gradient(self):
+        from oracle import filt, sens
+        u = self.u if self.u is not None else np.zeros(self.op.n_dof)
+        t = {}
+        t0 = time.perf_counter()
+        sens.compliance(self.op.f, u)
+        t["compliance"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        dc, _ = self.op.sensitivity(self.rho, u)
+        t["sensitivity"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        P = filt.filter_matrix(self.p.nx, self.p.ny, self.p.nz, self.p.rmin)
+        filt.apply_transpose(P, dc)
+        t["filter_build_and_transpose"] = time.perf_counter() - t0
+        self.phases = t
+        return sum(t.values())
+
+    def projected(self, t_iter: float, n_gpu_iters: int | None):
+        n_or = oracle_iters(self.cfg)
+        n = n_or if n_or else (n_gpu_iters or 1)
+        src = "the oracle's own count to 1e-10 (tests/golden)" if n_or else "the GPU solve's count (no oracle count recorded)"
+        return self.t_setup + n * t_iter + sum((self.phases or {}).values()), n, src
+
+    def describe(self, t_iter, n, src, t_eval):
+        ph = {k: round(v, 3) for k, v in (self.phases or {}).items()}
+        return (f"oracle (numpy/scipy fp64, as it stands) on {self.cfg}: setup {self.t_setup:.2f}s; "
+                f"{self.n_timed} timed Jacobi-PCG iterations (oracle.solve.pcg, matrix-free apply) at "
+                f"{t_iter:.4f}s each (median over {len(self.iter_times)} samples); gradient phases {ph}s; "
+                f"projected to {n} iterations ({src}) = {t_eval:.1f}s per evaluation")
+
+    def record(self, t_iter, n_gpu_iters=None):
+        t_eval, n, src = self.projected(t_iter, n_gpu_iters)
+        return {"value": 1.0 / t_eval, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
+                "threads": {"blas": blas_threads(), "scipy_sparse": 1, "numpy_elementwise": 1},
+                "cpu_model": cpu_model(), "kind": "oracle", "projected": True,
+                "sample": self.describe(t_iter, n, src, t_eval),
+                "phases_s": {"setup": self.t_setup, "pcg_iteration": t_iter, **(self.phases or {})},
+                "pcg_iterations_timed": self.n_timed, "pcg_iterations_projected": n}
+
+
+def cpu_baseline(cfg: str, n_gpu_iters: int, iters: int = 100):
+    """Our arm's cpu_baseline: the oracle on >= 100 PCG iterations of cfg (about a minute)."""
+    s = OracleSample(cfg)
+    s.gradient()
+    t_iter = s.iterate(iters)
+    return s.record(t_iter, n_gpu_iters)
 
 
 # ---------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The reference arm is the CPU oracle (the tier has no reference implementation): the
+    same config, metric and unit, each step a bounded sample (setup and the gradient phases
+    timed once, then a continuing share of >= 100 PCG iterations in total over the timed
+    steps), projected to a full evaluation with the oracle's own iteration count."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_2104_12282_b200 import inputs
     cfg = args.config
-    p = inputs.CONFIGS[cfg]
-    n_full = REF_ITERS.get(cfg)
+    s = OracleSample(cfg)
+    s.gradient()
+    n_step = max(5, -(-120 // max(args.steps, 1)))
+    for _ in range(args.warmup):
+        s.iterate(2)
+    s.iter_times, s.n_timed = [], 0
     times = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        v, desc, cores = oracle_sample(cfg, n_full, budget_iters=2)
-        if i >= args.warmup:
-            times.append(1.0 / v)
+    for _ in range(args.steps):
+        t_iter = s.iterate(n_step)
+        times.append(s.projected(t_iter, None)[0])
+    t_iter_med = float(np.median(s.iter_times))
+    rec = s.record(t_iter_med)
     tmed = float(np.median(times))
     val = 1.0 / tmed
+    rec["value"] = val
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmed * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, SURVEY §8 d1)",
-            "config": {"workload": p.name, "n_elem": p.n_elem, "n_dof": p.n_dof, "tol": args.tol},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "config": {"workload": s.p.name, "n_elem": s.p.n_elem, "n_dof": s.p.n_dof, "tol": args.tol},
+            "cpu_baseline": rec,
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-# PCG iteration counts used to project the oracle's bounded sample to a full evaluation
-# (the Jacobi-PCG recurrence is the same on both sides; counts agree to a few iterations).
-# cfg3: measured by libtomo at tol 1e-10 from x0 = 0 (10,485-10,488 across builds).
-REF_ITERS = {"cfg3": 10488}
 # DRAM bytes per launch of the dominant kernel from one `ncu --set full` capture
 # (dram__bytes_read.sum + dram__bytes_write.sum), see profiles/.
 TRAFFIC = {"cfg3": 272035584}  # r1 session 3 (committed kernel): DRAM read + write per launch (profiles/r1s3_pcg_kernel_ncu.json)
@@ -330,8 +412,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
-            v, desc, cores = oracle_sample(cfg, iters)
-            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+            cpu = cpu_baseline(cfg, iters)
         except Exception as ex:  # the baseline must never kill the bench line
             cpu = {"value": None, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                    "sample": f"failed: {ex!r}"}
@@ -354,10 +435,57 @@ def run_ours(args):
     return 0
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`--gpus N` without a launcher (WORLD_SIZE unset): start N replica ranks of this script,
+    one per GPU, with RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* set as torchrun would; rank 0
+    prints the JSON line. Returns the worst exit code."""
+    port = _free_port()
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    return max(abs(p.wait()) for p in procs)
+
+
+def run_mock(args):
+    """The launch / aggregation path without a GPU: rank r 'evaluates' by sleeping
+    10 ms x (r + 1) per step; gloo max-reduce of the time, whole-job value."""
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(0.01 * (rank + 1))
+    local_ms = (time.perf_counter() - t0) * 1e3
+    value, ms = replica_aggregate(args.steps, local_ms, world, torch_reduce_max("cpu"))
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms / args.steps, "mock": True,
+                          "local_ms": local_ms, "max_ms": ms}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.mock:
+        return run_mock(args)
     return run_ours(args)
 
 

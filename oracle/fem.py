@@ -84,8 +84,8 @@ def simp(rho, E0, Emin, penal):
     rho = np.asarray(rho, dtype=np.float64)
     # SPEC:118 requires rho in [0, 1]; reading R3 admits 1e-12 of rounding so that
     # the filtered density P x (row-stochastic P, x in [0, 1]) is accepted.
-    if np.any(rho < -1e-12) or np.any(rho > 1.0 + 1e-12):
-        raise ValueError("density outside [0, 1] (SPEC:118)")
+    if not np.all((rho >= -1e-12) & (rho <= 1.0 + 1e-12)):  # also rejects NaN
+        raise ValueError("density outside [0, 1] or NaN (SPEC:118)")
     return Emin + rho ** penal * (E0 - Emin)
 
 

@@ -45,7 +45,8 @@ class OracleProblem:
     def solve_direct(self, rho):
         return solve.direct_solve(self.Khat(rho), self.f)
 
-    def solve_pcg(self, rho, tol=1e-10, max_iters=200000, x0=None, use_csr=None):
+    def solve_pcg(self, rho, tol=1e-10, max_iters=200000, x0=None, use_csr=None, callback=None,
+                  callback_u=None):
         E = self.E(rho)
         if use_csr is None:
             use_csr = self._assemble and self.n_e <= 120_000
@@ -56,7 +57,8 @@ class OracleProblem:
             def op(v):
                 return fem.apply_matfree(v, E, self.KE, self.edof, self.fixed)
         dinv = 1.0 / fem.jacobi_diag(E, self.KE, self.edof, self.fixed)
-        return solve.pcg(op, dinv, self.f, x0=x0, tol=tol, max_iters=max_iters)
+        return solve.pcg(op, dinv, self.f, x0=x0, tol=tol, max_iters=max_iters, callback=callback,
+                         callback_u=callback_u)
 
     # ---- gradient pieces ------------------------------------------------
     @property

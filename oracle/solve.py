@@ -24,14 +24,16 @@ def direct_solve(Khat, f):
     return lu.solve(f)
 
 
-def pcg(apply_A, dinv, f, x0=None, tol=1e-10, max_iters=100000, callback=None):
+def pcg(apply_A, dinv, f, x0=None, tol=1e-10, max_iters=100000, callback=None,
+        callback_u=None):
     """Textbook Jacobi-preconditioned CG, in the order of SURVEY §8 a4:
 
         r0 = f - A x0, z0 = D^-1 r0, p0 = z0
         loop: q = A p; alpha = (r.z)/(p.q); u += alpha p; r -= alpha q;
               stop if ||r|| <= tol ||f||; z = D^-1 r; beta = (r.z)_new/(r.z); p = z + beta p
 
-    Returns (u, iterations, converged, ||r||/||f|| recursive).
+    Returns (u, iterations, converged, ||r||/||f|| recursive). callback(k, rel) and
+    callback_u(k, rel, u) are observation hooks (they must not modify u).
     pcg(identity) is pinned by tests (1 iteration), the 2x2 system of SPEC:176 too.
     """
     f = np.asarray(f, dtype=np.float64)
@@ -61,6 +63,8 @@ def pcg(apply_A, dinv, f, x0=None, tol=1e-10, max_iters=100000, callback=None):
         rnorm = np.linalg.norm(r)
         if callback is not None:
             callback(k, rnorm / fnorm)
+        if callback_u is not None:
+            callback_u(k, rnorm / fnorm, u)
         if rnorm <= tol * fnorm:
             return u, k, True, rnorm / fnorm
         z = dinv * r

@@ -3,7 +3,8 @@
   python scripts/make_golden.py cfg1   # 50-iteration SIMP/OC loop history (BASELINE configs[1])
   python scripts/make_golden.py cfg2   # tight oracle solve of the MBB half-beam (configs[2])
   python scripts/make_golden.py cfg0   # tight oracle solve of configs[0]
-  python scripts/make_golden.py cfg3   # tight oracle solve of configs[3], sampled (about an hour)
+  python scripts/make_golden.py cfg3   # tight oracle solve of configs[3], sampled (about 1.5 h)
+  python scripts/make_golden.py cfg4:0void07 cfg4:0uniform cfg4:1uniform cfg4:1void07
 
 The oracle solves with its own Jacobi-PCG to a relative residual of 1e-12 (reading A14:
 tighter than the 1e-10 the parity runs use), from x0 = 0.
@@ -44,51 +45,87 @@ def cfg1():
     print("cfg1 done", out["seconds"])
 
 
-def tight(name):
-    p = inputs.CONFIGS[name]
-    rho = inputs.density_for(name)
-    op = OracleProblem(p)
+class Snap:
+    """Observation hook of the oracle's PCG: keeps u at the first iteration whose recursive
+    residual is <= tol (the oracle's own solution at 1e-10, for A14's delta_floor)."""
+
+    def __init__(self, tol=1e-10):
+        self.tol, self.k, self.u = tol, None, None
+
+    def __call__(self, k, rel, u):
+        if self.k is None and rel <= self.tol:
+            self.k, self.u = k, u.copy()
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def tight(name, rho=None, p=None, store_full=True, use_csr=None):
+    """The oracle's own Jacobi-PCG to 1e-12 from x0 = 0, its snapshot at 1e-10 (the parity
+    tolerance) and A14's solver-noise floor delta_floor = ||x(1e-10) - x(1e-12)|| / ||x(1e-12)||
+    for x = u, dc, P^T dc."""
+    p = p or inputs.CONFIGS[name]
+    rho = inputs.density_for(name) if rho is None else rho
+    op = OracleProblem(p, assemble=use_csr is not False)
     t = time.time()
-    u, its, conv, rel = op.solve_pcg(rho, tol=1e-12)
-    _, its10, _, _ = op.solve_pcg(rho, tol=1e-10)
+    snap = Snap(1e-10)
+    u, its, conv, rel = op.solve_pcg(rho, tol=1e-12, max_iters=200000, use_csr=use_csr, callback_u=snap)
+    r = op.f - op.apply(rho, u)
+    rel_true = float(np.linalg.norm(r) / np.linalg.norm(op.f))
     c, dc, ce, dcf = op.evaluate(rho, u)
-    meta = {"citation": f"oracle Jacobi-PCG (tol 1e-12, x0 = 0) on BASELINE.json {name}; c = f^T u (Eq. 4), "
-                        "dc (Eq. 5 with (E0-Emin), reading A5), dcf = P^T dc. Written by scripts/make_golden.py.",
-            "c": c, "pcg_iters_1e-12": its, "pcg_iters_1e-10": its10, "converged": bool(conv),
-            "rel_res": rel, "seconds": time.time() - t}
-    with open(os.path.join(GOLD, f"{name}_solve.json"), "w") as f:
-        json.dump(meta, f, indent=1)
-    np.savez_compressed(os.path.join(GOLD, f"{name}_solve.npz"), u=u, dc=dc, dcf=dcf)
-    print(name, "done", meta)
+    c10, dc10, _, dcf10 = op.evaluate(rho, snap.u)
+    meta = {"citation": f"oracle Jacobi-PCG (tol 1e-12 recursive, x0 = 0) on BASELINE.json {p.name}; c = f^T u "
+                        "(Eq. 4), dc (Eq. 5 with (E0-Emin), reading A5), dcf = P^T dc; delta_floor = the oracle's "
+                        "own 1e-10 snapshot vs its 1e-12 solution (reading A14). Written by scripts/make_golden.py.",
+            "c": float(c), "c_1e-10": float(c10), "pcg_iters_1e-12": int(its), "pcg_iters_1e-10": snap.k,
+            "converged": bool(conv), "rel_res": float(rel), "rel_res_true": rel_true,
+            "delta_floor": {"u": _rel(snap.u, u), "dc": _rel(dc10, dc), "dcf": _rel(dcf10, dcf)},
+            "norm_u": float(np.linalg.norm(u)), "norm_dc": float(np.linalg.norm(dc)),
+            "norm_dcf": float(np.linalg.norm(dcf)), "seconds": time.time() - t}
+    if store_full:
+        with open(os.path.join(GOLD, f"{name}_solve.json"), "w") as f:
+            json.dump(meta, f, indent=1)
+        np.savez_compressed(os.path.join(GOLD, f"{name}_solve.npz"), u=u, dc=dc, dcf=dcf)
+    print(name, "done", meta, flush=True)
+    return meta, u, dc, dcf, snap.u
 
 
 def cfg3_sampled(n_sample=4096, seed=33):
     """configs[3] (4.35M DOFs): the oracle's own Jacobi-PCG to 1e-12 from x0 = 0 (about an
-    hour on 8-16 host cores), stored as c, the iteration count, the true residual, the
-    full-vector norms and seeded samples of u, dc and P^T dc ('full u parity
-    is run locally')."""
-    p = inputs.CFG3
-    rho = inputs.density_for("cfg3")
-    op = OracleProblem(p, assemble=False)
-    t = time.time()
-    u, its, conv, rel = op.solve_pcg(rho, tol=1e-12, max_iters=200000, use_csr=False)
-    r = op.f - op.apply(rho, u)
-    rel_true = float(np.linalg.norm(r) / np.linalg.norm(op.f))
-    c, dc, ce, dcf = op.evaluate(rho, u)
+    hour and a half on the host), stored as c, the iteration counts at 1e-10 and 1e-12, the
+    true residual, the full-vector norms, delta_floor and seeded samples of u, dc and P^T dc
+    ('full u parity is run locally')."""
+    meta, u, dc, dcf, _ = tight("cfg3", store_full=False, use_csr=False)
+    op = OracleProblem(inputs.CFG3, assemble=False)
     rng = np.random.default_rng(seed)
     idof = np.sort(rng.choice(op.n_dof, n_sample, replace=False))
     iel = np.sort(rng.choice(op.n_e, n_sample, replace=False))
-    meta = {"citation": "oracle Jacobi-PCG (tol 1e-12 recursive, x0 = 0, matrix-free apply) on BASELINE.json "
-                        "configs[3]; c = f^T u (Eq. 4), dc (Eq. 5, reading A5), dcf = P^T dc; seeded samples. "
-                        "Written by scripts/make_golden.py cfg3.",
-            "c": float(c), "pcg_iters_1e-12": int(its), "converged": bool(conv), "rel_res_recursive": float(rel),
-            "rel_res_true": rel_true, "norm_u": float(np.linalg.norm(u)), "norm_dc": float(np.linalg.norm(dc)),
-            "norm_dcf": float(np.linalg.norm(dcf)), "seconds": time.time() - t,
-            "dof_idx": idof.tolist(), "u": u[idof].tolist(), "elem_idx": iel.tolist(),
-            "dc": dc[iel].tolist(), "dcf": dcf[iel].tolist()}
+    meta.update({"dof_idx": idof.tolist(), "u": u[idof].tolist(), "elem_idx": iel.tolist(),
+                 "dc": dc[iel].tolist(), "dcf": dcf[iel].tolist()})
     with open(os.path.join(GOLD, "cfg3_sampled.json"), "w") as f:
         json.dump(meta, f)
-    print("cfg3 done", {k: meta[k] for k in ("c", "pcg_iters_1e-12", "rel_res_true", "seconds")})
+    print("cfg3 done", {k: meta[k] for k in ("c", "pcg_iters_1e-12", "pcg_iters_1e-10", "rel_res_true",
+                                              "seconds")})
+
+
+def cfg4(idx_variant, n_sample=4096, seed=44):
+    """configs[4] full-solve parity grids (32^3 and 64^3), void 0.7 and uniform
+    0.5. 32^3: full vectors; 64^3: sampled like cfg3."""
+    idx, variant = int(idx_variant[0]), idx_variant[1:]
+    p = inputs.cfg4(idx)
+    rho = inputs.density_void07(p) if variant == "void07" else inputs.density_uniform(p, 0.5)
+    name = f"cfg4{'abcde'[idx]}_{variant}"
+    full = p.n_elem <= 40_000
+    meta, u, dc, dcf, _ = tight(name, rho=rho, p=p, store_full=full, use_csr=True)
+    if not full:
+        rng = np.random.default_rng(seed)
+        idof = np.sort(rng.choice(u.size, n_sample, replace=False))
+        iel = np.sort(rng.choice(dc.size, n_sample, replace=False))
+        meta.update({"dof_idx": idof.tolist(), "u": u[idof].tolist(), "elem_idx": iel.tolist(),
+                     "dc": dc[iel].tolist()})
+        with open(os.path.join(GOLD, f"{name}_sampled.json"), "w") as f:
+            json.dump(meta, f)
 
 
 if __name__ == "__main__":
@@ -97,5 +134,7 @@ if __name__ == "__main__":
             cfg1()
         elif a == "cfg3":
             cfg3_sampled()
+        elif a.startswith("cfg4:"):   # cfg4:0void07, cfg4:1uniform, ...
+            cfg4(a.split(":", 1)[1])
         else:
             tight(a)

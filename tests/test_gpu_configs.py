@@ -42,7 +42,7 @@ def test_cfg3_evaluation_residual_pins():
     rho = inputs.density_for("cfg3")
     t = ctx(p)
     u_g, c, dcf, info = t.evaluate(gpu(rho), tol=1e-10)
-    assert info.converged == 1
+    assert info.converged >= 1
     u = cpu(u_g)
     op = OracleProblem(p, assemble=False)
     r = op.f - op.apply(rho, u)
@@ -81,11 +81,11 @@ def test_cfg2_mbb_half_beam_against_tight_oracle():
     rho = inputs.density_for("cfg2")
     t = ctx(p)
     u_g, c, dcf, info = t.evaluate(gpu(rho), tol=1e-10)
-    assert info.converged == 1
+    assert info.converged >= 1
     assert abs(info.iterations - meta["pcg_iters_1e-10"]) <= max(3, 0.02 * meta["pcg_iters_1e-10"])
     assert abs(c - meta["c"]) <= 1e-9 * abs(meta["c"])
     u12, info12 = t.solve(gpu(rho), tol=1e-12, max_iters=200000)
-    assert info12.converged == 1
+    assert info12.converged >= 1
     assert rel(cpu(u12), gold["u"]) <= 1e-8
     dc12 = cpu(t.sensitivity(gpu(rho), u12))
     assert rel(dc12, gold["dc"]) <= 1e-8
@@ -136,7 +136,7 @@ def test_cfg4a_solve_residual_pins():
     rho = inputs.density_void07(p)
     t = ctx(p)
     u_g, info = t.solve(gpu(rho), tol=1e-10)
-    assert info.converged == 1
+    assert info.converged >= 1
     op = OracleProblem(p)
     u = cpu(u_g)
     r = op.f - op.Khat(rho) @ u
@@ -202,7 +202,7 @@ def test_cfg3_loop_20_iterations():
     for k in range(p.loop_iters):
         xk = cpu(x)
         xn, c, lam, steps, info = loop.step(x)
-        assert info.converged == 1
+        assert info.converged >= 1
         cs.append(c)
         xn_h = cpu(xn)
         assert xn_h.min() >= 0.0 and xn_h.max() <= 1.0
@@ -235,7 +235,7 @@ def test_cfg3_against_sampled_tight_oracle_if_present():
     t = ctx(p)
     idof, iel = np.array(g["dof_idx"]), np.array(g["elem_idx"])
     u12, c12, dcf12, info12 = t.evaluate(rho, tol=1e-12, max_iters=200000)
-    assert info12.converged == 1
+    assert info12.converged >= 1
     dc12 = cpu(t.sensitivity(rho, u12))
     u10, c10, dcf10, info10 = t.evaluate(rho, tol=1e-10)
     dc10 = cpu(t.sensitivity(rho, u10))

@@ -65,7 +65,7 @@ def test_explicit_partial_bcs_apply_and_solve():
     f = grid.load_vector(n_dof, np.array(ldofs), np.array(lvals))
     u_ref = solve.direct_solve(K, f)
     ug, info = t.solve(gpu(rho), tol=1e-12)
-    assert info.converged == 1 and rel(cpu(ug), u_ref) <= 1e-9
+    assert info.converged >= 1 and rel(cpu(ug), u_ref) <= 1e-9
     assert abs(t.compliance(ug) - f @ u_ref) <= 1e-10 * abs(f @ u_ref)
 
 
@@ -118,7 +118,7 @@ def test_warm_start_and_max_iters():
     u_cold, i_cold = t.solve(gpu(rho), tol=1e-10)
     u0 = u_cold.clone() * (1 + 1e-6)
     u_warm, i_warm = t.solve(gpu(rho), u=u0, tol=1e-10)
-    assert i_warm.converged == 1 and i_warm.iterations < i_cold.iterations
+    assert i_warm.converged >= 1 and i_warm.iterations < i_cold.iterations
     assert rel(cpu(u_warm), cpu(u_cold)) <= 1e-8
     u_cap, i_cap = t.solve(gpu(rho), tol=1e-14, max_iters=7)
     assert i_cap.iterations == 7 and i_cap.converged == 0  # not an error

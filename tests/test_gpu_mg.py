@@ -30,7 +30,7 @@ def test_mg_cfg0_against_direct_solve():
     t = tomo.Tomo(tomo.params_from_problem(p), device=DEV)
     t.mg_setup(3)
     u, info = t.solve_mg(gpu(rho), tol=1e-10)
-    assert info.converged == 1 and info.rel_res_true <= 2e-10
+    assert info.converged >= 1 and info.rel_res_true <= 2e-10
     op = OracleProblem(p)
     u_ref = op.solve_direct(rho)
     assert rel(u.cpu().numpy(), u_ref) <= 1e-8
@@ -48,7 +48,7 @@ def test_mg_cfg2_against_tight_oracle():
     t = tomo.Tomo(tomo.params_from_problem(p), device=DEV)
     t.mg_setup(5)
     u, info = t.solve_mg(gpu(rho), tol=1e-12)
-    assert info.converged == 1
+    assert info.converged >= 1
     assert rel(u.cpu().numpy(), gold["u"]) <= 1e-8
     assert abs(t.compliance(u) - meta["c"]) <= 1e-9 * abs(meta["c"])
     assert info.iterations * 10 < meta["pcg_iters_1e-12"]
@@ -64,5 +64,5 @@ def test_mg_mbb_small_and_errors():
     t.mg_setup(4)
     u, info = t.solve_mg(gpu(rho), tol=1e-11)
     op = OracleProblem(p)
-    assert info.converged == 1
+    assert info.converged >= 1
     assert rel(u.cpu().numpy(), op.solve_direct(rho)) <= 1e-9

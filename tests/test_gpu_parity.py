@@ -125,7 +125,7 @@ def test_cfg0_solve_parity(cfg0):
     t = ctx_for(p)
     u, info = t.solve(gpu(rho), tol=1e-10)
     u = cpu(u)
-    assert info.converged == 1
+    assert info.converged >= 1
     assert info.rel_res_true <= 2e-10
     assert abs(info.iterations - its_ref) <= max(2, 0.02 * its_ref)
     assert rel(u, u_ref) <= 1e-8
@@ -176,7 +176,13 @@ def test_filter_parity(nx, ny, nz, rmin):
     assert rel(cpu(t.volume_grad()), filt.volume_gradient(P)) <= 1e-14
 
 
-def test_oc_parity_random_instances():
+def test_oc_parity_1000_random_instances():
+    """SPEC.md l.636 (acceptance criterion 3: 1,000 random (z, g, dV) instances) through the
+    k_oc kernel against oracle/oc.py: box and move limits, the volume target within 1e-6 when
+    reachable, lambda to 1e-13 and x to 1e-12. The two sides sum the volume in different
+    orders, so a bisection decision can flip where V(lm) is within rounding of the target
+    (reading A17): every instance whose lambda differs is checked to be such a flip - the
+    oracle's own volume at the GPU's lambda equals the target to 1e-12."""
     rng = np.random.default_rng(0)
     nx, ny, nz = 8, 6, 5
     p = inputs.Problem("o", nx, ny, nz, rmin=1.5)
@@ -184,20 +190,35 @@ def test_oc_parity_random_instances():
     P = filt.filter_matrix(nx, ny, nz, 1.5)
     dv = filt.volume_gradient(P)
     dv_g = t.volume_grad()
+    assert rel(cpu(dv_g), dv) <= 1e-14
     n = nx * ny * nz
-    flips = 0
-    for inst in range(40):
-        x = rng.uniform(0.01, 1.0, n)
+    flips = unreachable = 0
+    for inst in range(1000):
+        x = rng.uniform(0.0, 1.0, n)
         g = -rng.uniform(0, 1, n) ** 3 * 10 ** rng.uniform(-3, 3)
-        vf = rng.uniform(0.1, 0.6)
-        xn_ref, lam_ref, steps_ref, _ = ooc.oc_update(x, g, dv, P, vf, 0.2, 0.5)
-        xn, lam, steps = t.oc_update(gpu(x), gpu(g), dv_g, vf, 0.2, 0.5)
-        # tight bisection (A17): a decision flip moves lambda by at most the final bracket
-        assert abs(lam - lam_ref) <= 1e-13 * lam_ref
-        assert np.max(np.abs(cpu(xn) - xn_ref)) <= 1e-12
+        if inst % 10 == 0:
+            g[rng.integers(0, n, 5)] = 0.0  # zero drive on some elements
+        vf = rng.uniform(0.05, 0.95)
+        move = rng.choice([0.05, 0.2, 0.5])
+        xn_ref, lam_ref, steps_ref, _ = ooc.oc_update(x, g, dv, P, vf, move, 0.5)
+        xn, lam, steps = t.oc_update(gpu(x), gpu(g), dv_g, vf, move, 0.5)
+        xh = cpu(xn)
+        assert xh.min() >= 0.0 and xh.max() <= 1.0
+        assert np.all(np.abs(xh - x) <= move * (1 + 1e-15))
         assert (steps < 0) == (steps_ref < 0)
-        flips += lam != lam_ref
-    assert flips <= 40
+        if steps > 0:
+            assert abs(float(np.sum(P @ xh)) - vf * n) <= 1e-6 * vf * n
+        else:
+            unreachable += 1
+        assert abs(lam - lam_ref) <= 1e-13 * lam_ref
+        assert np.max(np.abs(xh - xn_ref)) <= 1e-12
+        if lam != lam_ref:
+            flips += 1
+            v_at = float(np.sum(P @ ooc.x_new(x, g, dv, lam, move, 0.5)))
+            assert abs(v_at - vf * n) <= 1e-12 * vf * n, (inst, v_at, vf * n)
+    print(f"OC 1000 instances: {flips} lambda flips (all at rounding-level volume decisions), "
+          f"{unreachable} unreachable targets")
+    assert flips <= 500
 
 
 # ------------------------------------------------------------------ edges and errors

@@ -40,7 +40,7 @@ def test_cfg2_solve_any_schedule(env, monkeypatch):
     t = _ctx(p, monkeypatch, **env)
     rho = torch.tensor(inputs.density_for("cfg2"), dtype=torch.float64, device=DEV)
     u, info = t.solve(rho, tol=1e-12, max_iters=200000)
-    assert info.converged == 1
+    assert info.converged >= 1
     u = u.cpu().numpy()
     assert np.linalg.norm(u - gold["u"]) <= 1e-8 * np.linalg.norm(gold["u"])
     # the count depends on rounding (partial sums grouped per block), not on the schedule
@@ -55,7 +55,7 @@ def test_cfg4e_multiwave_solve_residual_pin(monkeypatch):
     t = _ctx(p, monkeypatch)
     rho_np = inputs.density_uniform(p, 0.5)
     u_g, info = t.solve(torch.tensor(rho_np, dtype=torch.float64, device=DEV), tol=1e-3)
-    assert info.converged == 1 and info.iterations > 10
+    assert info.converged >= 1 and info.iterations > 10
     op = OracleProblem(p, assemble=False)
     u = u_g.cpu().numpy()
     r = op.f - op.apply(rho_np, u)

@@ -66,7 +66,7 @@ def test_coarse_solve_cfg0_nb2_against_direct():
     uc, info = tc.solve(zc_g, tol=1e-10)
     zc, K, f = _oracle_coarse(dims, bc, nb, rho)
     u_ref = solve.direct_solve(K, f)
-    assert info.converged == 1
+    assert info.converged >= 1
     assert rel(cpu(uc), u_ref) <= 1e-8
     c_ref = sens.compliance(f, u_ref)
     assert abs(tc.compliance(uc) - c_ref) <= 1e-9 * abs(c_ref)
@@ -89,7 +89,7 @@ def test_coarse_cfg3_nb4_residual_pins():
     t = tomo.Tomo(tomo.params_from_problem(inputs.CFG3), device=DEV)
     tc = t.coarse(nb)
     uc, info = tc.solve(t.coarsen(gpu(rho), nb), tol=1e-10)
-    assert info.converged == 1
+    assert info.converged >= 1
     zc, K, f = _oracle_coarse(dims, bc, nb, rho)
     u = cpu(uc)
     r = np.linalg.norm(f - K @ u) / np.linalg.norm(f)

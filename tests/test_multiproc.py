@@ -53,3 +53,19 @@ def test_reference_arm_nonzero_rank_exits_quietly():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2"],
                        env=env, capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_bench_self_launches_n_ranks():
+    """`bench.py --gpus 2` with WORLD_SIZE unset starts 2 replica ranks itself;
+    --mock replaces the GPU evaluation by a per-rank sleep (rank 1 slower): n_gpus = 2 and the
+    time is the max over ranks."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--mock",
+                        "--steps", "5", "--warmup", "0"], env=env, capture_output=True, text=True,
+                       timeout=180)
+    assert r.returncode == 0, r.stderr[-2000:]
+    import json
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["mock"] is True
+    assert line["max_ms"] >= line["local_ms"] and line["max_ms"] >= 5 * 20.0  # rank 1: 20 ms/step
+    assert abs(line["value"] - 2 * 5 / (line["max_ms"] * 1e-3)) < 1e-6 * line["value"]
