@@ -221,6 +221,10 @@ int64_t tomo_launch_count(const tomo_ctx* ctx);
  * sustained FP64 FMA rate (GFLOP/s, FMA = 2 flop) and the per-launch mean time of the
  * PCG kernels of the last tomo_solve measured with CUDA events on the bound stream.      */
 int tomo_bench_dfma(tomo_ctx* ctx, double* gflops_out, double* ms_out);
+/* Residual history of the next solves (diagnostics): while set, launch k of
+ * every PCG solve writes d_hist[k] = r_k^T r_k (k < n; the relative residual is
+ * sqrt(d_hist[k]) / ||f||). d_hist: caller-owned device buffer of n doubles; n = 0 stops.  */
+int tomo_set_history(tomo_ctx* ctx, double* d_hist, int n);
 /* PCG loop execution (default 1): 1 = the whole loop as one CUDA graph with a conditional
  * WHILE node (one launch and one read-back per solve); 0 = host-batched launches of the
  * same kernel (what ncu can profile: kernels inside conditional graphs are not captured). */

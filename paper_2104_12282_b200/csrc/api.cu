@@ -370,7 +370,7 @@ extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, doubl
   for (int64_t d : c->load_dofs) {
     const long long n = d / 3;
     const int i = (int)(n % g.nnx), j = (int)((n / g.nnx) % g.nny), k = (int)(n / ((long long)g.nnx * g.nny));
-    c->load_dofs_pad.push_back(3 * node_pad(g, i, j, k) + d % 3);
+    c->load_dofs_pad.push_back(dof_pad(g, i, j, k, (int)(d % 3)));
   }
   double ff = 0;
   for (double v : c->load_vals) ff += v * v;
@@ -448,25 +448,26 @@ namespace {
 // operator launch variants: maps over the padded internal vectors
 int build_op_args(tomo_ctx* c) {
   const Grid& g = c->g;
-  const uint64_t rowv = 24ull * g.nnx_pad, planev = rowv * g.nny;
+  // row-SoA vectors: a 3-D map over (x, 3 * y + component, z), sub-row pitch 8 nnx_pad bytes
+  const uint64_t rowv = 8ull * g.nnx_pad, planev = 3 * rowv * g.nny;
   const uint64_t rown = 8ull * g.nnx_pad, planen = rown * g.nny;
   const uint64_t rowm = (uint64_t)g.mp, planem = rowm * g.nny;
   const uint64_t rowe = 8ull * g.nx_pad, planee = rowe * g.ny;
   const CUtensorMapDataType F64 = CU_TENSOR_MAP_DATA_TYPE_FLOAT64, U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
-  const uint32_t inw = 3 * (OP_OX + 2) + 2, inh = OP_BY + 1;  // boxes widened: aligned starts
+  const uint32_t inw = OP_TX + 2, inh = OP_BY + 1;  // boxes widened: aligned starts
   CUtensorMap tm_u, tm_uown, tm_r[2], tm_q[2], tm_p[2], tm_dinv, tm_mask, tm_E;
   int rc;
-  auto vec = [&](CUtensorMap* tm, double* base, uint32_t b0, uint32_t b1) {
-    return make_map(c, tm, F64, base, 3ull * g.nnx, g.nny, g.nnz, rowv, planev, b0, b1);
+  auto vec = [&](CUtensorMap* tm, double* base, uint32_t b0, uint32_t rows) {
+    return make_map(c, tm, F64, base, g.nnx, 3ull * g.nny, g.nnz, rowv, planev, b0, 3 * rows);
   };
   if ((rc = vec(&tm_u, c->u(), inw, inh))) return rc;
-  if ((rc = vec(&tm_uown, c->u(), 3 * OP_OX, OP_OY))) return rc;
+  if ((rc = vec(&tm_uown, c->u(), inw, OP_OY))) return rc;
   for (int i = 0; i < 2; ++i) {
     if ((rc = vec(&tm_r[i], c->r(i), inw, inh))) return rc;
     if ((rc = vec(&tm_q[i], c->q(i), inw, inh))) return rc;
     if ((rc = vec(&tm_p[i], c->p(i), inw, inh))) return rc;
   }
-  if ((rc = make_map(c, &tm_dinv, F64, c->dinv(), g.nnx, g.nny, g.nnz, rown, planen, OP_OX + 4, inh))) return rc;
+  if ((rc = make_map(c, &tm_dinv, F64, c->dinv(), g.nnx, g.nny, g.nnz, rown, planen, inw, inh))) return rc;
   if ((rc = make_map(c, &tm_mask, U8, c->dmask(), g.nnx, g.nny, g.nnz, rowm, planem, 48, inh))) return rc;
   if ((rc = make_map(c, &tm_E, F64, c->E(), g.nx, g.ny, g.nz, rowe, planee, 32, OP_BY))) return rc;
   OpArgs base{};
@@ -983,6 +984,17 @@ extern "C" int tomo_bench_dfma(tomo_ctx* c, double* gflops_out, double* ms_out) 
   return TOMO_OK;
 }
 
+extern "C" int tomo_set_history(tomo_ctx* c, double* d_hist, int n) {
+  if (int rc = need_bound(c)) return rc;
+  if (n < 0 || (n > 0 && !check_ptr(d_hist))) return fail(c, TOMO_EINVAL, "bad history buffer");
+  Scal* s = c->scal();
+  double* h = n > 0 ? d_hist : nullptr;
+  CK(c, cudaMemcpyAsync(&s->hist, &h, sizeof(h), cudaMemcpyHostToDevice, c->st));
+  CK(c, cudaMemcpyAsync(&s->hist_n, &n, sizeof(n), cudaMemcpyHostToDevice, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return TOMO_OK;
+}
+
 extern "C" int tomo_set_graph(tomo_ctx* c, int on) {
   if (!c) return TOMO_EINVAL;
   c->use_graph = on != 0;
@@ -1093,12 +1105,12 @@ int mg_levels_possible(const Grid& g) {
 // APPLY with an arbitrary (padded, fine-level) input buffer: maps built at tomo_mg_bind
 int mg_build_maps(tomo_ctx* c) {
   const Grid& g = c->g;
-  const uint64_t rowv = 24ull * g.nnx_pad, planev = rowv * g.nny;
-  const uint32_t inw = 3 * (OP_OX + 2) + 2, inh = OP_BY + 1;
+  const uint64_t rowv = 8ull * g.nnx_pad, planev = 3 * rowv * g.nny;  // row-SoA (dof_pad)
+  const uint32_t inw = OP_TX + 2, inh = 3 * (OP_BY + 1);
   CUtensorMap tP, tZ;
   auto P = [&](size_t off) { return reinterpret_cast<double*>(c->mg_ws + off); };
-  if (int rc = make_map(c, &tP, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, P(c->mg_off_P), 3ull * g.nnx, g.nny, g.nnz, rowv, planev, inw, inh)) return rc;
-  if (int rc = make_map(c, &tZ, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, P(c->mg_off_Z), 3ull * g.nnx, g.nny, g.nnz, rowv, planev, inw, inh)) return rc;
+  if (int rc = make_map(c, &tP, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, P(c->mg_off_P), g.nnx, 3ull * g.nny, g.nnz, rowv, planev, inw, inh)) return rc;
+  if (int rc = make_map(c, &tZ, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, P(c->mg_off_Z), g.nnx, 3ull * g.nny, g.nnz, rowv, planev, inw, inh)) return rc;
   c->op_apply_P = c->op_apply_u;
   c->op_apply_P.tm_in = tP;
   c->op_apply_P.out = P(c->mg_off_Q);

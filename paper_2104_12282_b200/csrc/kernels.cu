@@ -40,32 +40,36 @@ constexpr int OY = OP_OY;              // output nodes per tile along y
 constexpr int NS = OP_NS;              // pipeline stages
 constexpr int NR = BY + 1;             // node rows per tile (warp w stages rows w, w+1)
 constexpr int ER = BY;                 // element rows per tile (one per warp)
-constexpr int OWN_W = 3 * OX;          // 90 doubles per owned row
-constexpr int OWN_N = OWN_W * OY;      // 540
+// Internal vectors are row-SoA (tomo_internal.h dof_pad): a node row is 3 component
+// sub-rows of nnx_pad doubles, so lane tx <-> node i0-1+tx reads and writes one component
+// of 32 consecutive nodes per instruction (coalesced global stores, conflict-free smem).
 // TMA boxes. The innermost box start must be 16-byte aligned (measured on this B200: an
 // 8-byte-aligned start faults with "illegal instruction"), so every box starts at the
 // aligned-down coordinate and is widened; smem reads add the per-block offset.
-constexpr int VB_W = 3 * (OX + 2) + 2; // 98 doubles: vector rows (start offset 0..1)
-constexpr int DB_W = OX + 4;           // 34 doubles: Jacobi rows (start offset 0..1)
+constexpr int VB_W = TX + 2;           // 34 doubles per component sub-row (start offset 0..1)
+constexpr int VB_R = 3 * NR;           // 27 sub-rows: node rows j0-1 .. j0+BY-1, 3 components
+constexpr int UB_R = 3 * OY;           // 21 sub-rows: owned node rows j0 .. j0+OY-1 (u, PCG)
+constexpr int DB_W = TX + 2;           // 34 doubles: Jacobi rows (start offset 0..1)
 constexpr int MB_W = 48;               // 48 bytes: mask rows (start offset 0..15)
 constexpr int E_W = 32;                // element box width (start offset 0..1, 31 used)
 constexpr int GSN = 12;                // top face carried as Walsh face modes
 // stage layout in doubles, every piece 128-byte aligned
 constexpr int al16(int n) { return (n + 15) & ~15; }  // doubles -> multiple of 128 B
 constexpr int R_OFF = 0;                                       // r_{k-1} (APPLY: u)
-constexpr int QO_OFF = R_OFF + al16(VB_W * NR);                // q_{k-1}
-constexpr int PO_OFF = QO_OFF + al16(VB_W * NR);               // p_{k-1}
-constexpr int UO_OFF = PO_OFF + al16(VB_W * NR);               // u, owned box
-constexpr int DI_OFF = UO_OFF + al16(OWN_N);                   // D^-1
+constexpr int QO_OFF = R_OFF + al16(VB_W * VB_R);              // q_{k-1}
+constexpr int PO_OFF = QO_OFF + al16(VB_W * VB_R);             // p_{k-1}
+constexpr int UO_OFF = PO_OFF + al16(VB_W * VB_R);             // u, owned rows
+constexpr int DI_OFF = UO_OFF + al16(VB_W * UB_R);             // D^-1
 constexpr int EE_OFF = DI_OFF + al16(DB_W * NR);               // E
 constexpr int MK_OFF = EE_OFF + al16(E_W * ER);                // mask bytes
 constexpr int STAGE = MK_OFF + al16((MB_W * NR + 7) / 8);
-constexpr unsigned BYTES_PCG = 8u * (3 * VB_W * NR + OWN_N + DB_W * NR + E_W * ER) + MB_W * NR;
-constexpr unsigned BYTES_APPLY = 8u * (VB_W * NR + E_W * ER) + MB_W * NR;
+constexpr unsigned BYTES_PCG =
+    8u * (3 * VB_W * VB_R + VB_W * UB_R + DB_W * NR + E_W * ER) + MB_W * NR;
+constexpr unsigned BYTES_APPLY = 8u * (VB_W * VB_R + E_W * ER) + MB_W * NR;
 // APPLY stages hold only u, E and the mask (9.7 KB): more of them fit, and they are needed
 // because a stage carries too few bytes to cover DRAM latency with two
 constexpr int NS_A = OP_NS_APPLY;
-constexpr int EE_OFF_A = al16(VB_W * NR);
+constexpr int EE_OFF_A = al16(VB_W * VB_R);
 constexpr int MK_OFF_A = EE_OFF_A + al16(E_W * ER);
 constexpr int STAGE_A = MK_OFF_A + al16((MB_W * NR + 7) / 8);
 
@@ -289,15 +293,14 @@ __device__ __forceinline__ void corner_offset(int a, int& ax, int& ay, int& az) 
 // ------------------------------------------------------------------ operator / K_A
 // box starts (aligned down) of one block's tiles; offsets are the smem shifts
 struct TileOrigin {
-  int xv, xd, xm, xe;  // aligned starts: vector (doubles), Jacobi, mask (bytes), element
-  int ov, od, om, oe;  // offsets of node i0-1 (element i0-1) inside the boxes
+  int xv, xm, xe;  // aligned starts: vector / Jacobi (doubles), mask (bytes), element
+  int ov, om, oe;  // offsets of node i0-1 (element i0-1) inside the boxes
 };
 
 __device__ __forceinline__ TileOrigin tile_origin(int i0) {
   TileOrigin o;
-  const int sv = 3 * (i0 - 1), sn = i0 - 1;
-  o.xv = sv & ~1; o.ov = sv - o.xv;
-  o.xd = sn & ~1; o.od = sn - o.xd;
+  const int sn = i0 - 1;
+  o.xv = sn & ~1; o.ov = sn - o.xv;
   o.xm = sn & ~15; o.om = sn - o.xm;
   o.xe = sn & ~1; o.oe = sn - o.xe;
   return o;
@@ -308,12 +311,13 @@ __device__ __forceinline__ void issue_plane(const OpArgs& a, double* stg, uint64
                                             const TileOrigin& o, int i0, int j0, int kq) {
   using L = Lay<MODE>;
   mbar_expect_tx(bar, L::bytes);
-  tma_load_3d(stg + R_OFF, &a.tm_in, o.xv, j0 - 1, kq, bar);
+  // vector boxes: sub-rows 3 (j0-1) .. 3 (j0+BY) - 1 (row -3..-1 = node row -1: OOB, zeros)
+  tma_load_3d(stg + R_OFF, &a.tm_in, o.xv, 3 * (j0 - 1), kq, bar);
   if (MODE == OP_PCG) {
-    tma_load_3d(stg + QO_OFF, &a.tm_qold, o.xv, j0 - 1, kq, bar);
-    tma_load_3d(stg + PO_OFF, &a.tm_pold, o.xv, j0 - 1, kq, bar);
-    tma_load_3d(stg + UO_OFF, &a.tm_uown, 3 * i0, j0, kq, bar);
-    tma_load_3d(stg + DI_OFF, &a.tm_dinv, o.xd, j0 - 1, kq, bar);
+    tma_load_3d(stg + QO_OFF, &a.tm_qold, o.xv, 3 * (j0 - 1), kq, bar);
+    tma_load_3d(stg + PO_OFF, &a.tm_pold, o.xv, 3 * (j0 - 1), kq, bar);
+    tma_load_3d(stg + UO_OFF, &a.tm_uown, o.xv, 3 * j0, kq, bar);
+    tma_load_3d(stg + DI_OFF, &a.tm_dinv, o.xv, j0 - 1, kq, bar);
   }
   tma_load_3d(stg + L::mk, &a.tm_mask, o.xm, j0 - 1, kq, bar);
   tma_load_3d(stg + L::ee, &a.tm_E, o.xe, j0 - 1, kq - 1, bar);  // element plane kq-1
@@ -403,18 +407,15 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   const int gi = i0 - 1 + tx, gj = j0 + ty;
   const bool own_row = ty < OY && gj <= g.ny;
   const bool mine = own_row && tx >= 1 && tx <= OX && gi <= g.nx;
-  const int g_row = 3 * i0 + rowd * gj;                  // owned segment, + planed * plane
-  const int own_lim = 3 * min(OX, g.nx - i0 + 1);        // doubles of the segment in the domain
-  const int fvb = ty * VB_W + org.ov + 3 * tx;           // node rows ty (b) and ty+1 (o) in the
-  const int fvo = fvb + VB_W;                            // vector box
-  const int fdb = ty * DB_W + org.od + tx, fdo = fdb + DB_W;
+  const int g_own = gi + rowd * gj;                      // node (gi, gj), component 0, plane 0
+  // smem offsets: component-0 sub-row of node rows ty (b) and ty+1 (o) in the vector box,
+  // lane tx at node i0-1+tx; component c adds c * VB_W
+  const int fvb = 3 * ty * VB_W + org.ov + tx;
+  const int fvo = fvb + 3 * VB_W;
+  const int fuo = 3 * ty * VB_W + org.ov + tx;           // node row ty+1 in the owned-u box
+  const int fdb = ty * DB_W + org.ov + tx, fdo = fdb + DB_W;
   const int fmb = ty * MB_W + org.om + tx, fmo = fmb + MB_W;
   const int fe = ty * E_W + org.oe + tx;                 // element (tx, ty)
-  // owned-segment commit (PCG): stage offsets of node row ty+1 from node i0, and the node
-  // (within the segment) of positions tx, tx+32, tx+64
-  const int fown = (ty + 1) * VB_W + org.ov + 3;
-  const int down = (ty + 1) * DB_W + org.od + 1;
-  const int nd3[3] = {tx / 3, (tx + 32) / 3, (tx + 64) / 3};
 
   // state carried from one node plane to the next; K_hat u uses the two copies ping-pong (the
   // loop unrolled by two) so that nothing is copied between registers at the end of a step
@@ -446,36 +447,31 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
     if (MODE == OP_PCG) {
       const double dib = stg[DI_OFF + fdb];
       N.pdi = stg[DI_OFF + fdo];
+      double pold_o[3], ro[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double rb = fma(-alpha_prev, stg[QO_OFF + fvb + c], stg[R_OFF + fvb + c]);
-        vb[c] = fma(beta, stg[PO_OFF + fvb + c], dib * rb);
-        const double ro = fma(-alpha_prev, stg[QO_OFF + fvo + c], stg[R_OFF + fvo + c]);
-        N.pz[c] = N.pdi * ro;
-        vo[c] = fma(beta, stg[PO_OFF + fvo + c], N.pz[c]);
+        const int cb = fvb + c * VB_W, co = fvo + c * VB_W;
+        const double rb = fma(-alpha_prev, stg[QO_OFF + cb], stg[R_OFF + cb]);
+        vb[c] = fma(beta, stg[PO_OFF + cb], dib * rb);
+        ro[c] = fma(-alpha_prev, stg[QO_OFF + co], stg[R_OFF + co]);
+        N.pz[c] = N.pdi * ro[c];
+        pold_o[c] = stg[PO_OFF + co];
+        vo[c] = fma(beta, pold_o[c], N.pz[c]);
       }
-      // owned updates of node row o, coalesced: lane l handles doubles l, l+32, l+64 of the
-      // 90-double owned segment (nodes i0..i0+29), recomputed from the stage
-      if (own_row && kn >= kbeg && kn < kend) {
-        const int grow = g_row + planed * kn;
+      // owned updates of node row o (r_k, p_k, u_k): one component of 30 consecutive nodes
+      // per store instruction (row-SoA layout)
+      if (mine && kn >= kbeg && kn < kend) {
+        const int go = g_own + planed * kn;
         double rz = 0.0, rr = 0.0;
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const int pos = tx + 32 * q;  // position in the owned segment
-          if (pos < own_lim) {
-            const int f = fown + pos;
-            const double di = stg[DI_OFF + down + nd3[q]];
-            const double po = stg[PO_OFF + f];
-            const double rn = fma(-alpha_prev, stg[QO_OFF + f], stg[R_OFF + f]);
-            const double z = di * rn;
+        for (int c = 0; c < 3; ++c) {
 #ifndef TOMO_EXP_NO_COMMIT_STORE  // timing experiment only
-            a.rnew[grow + pos] = rn;
-            a.pnew[grow + pos] = fma(beta, po, z);
-            a.u[grow + pos] = fma(alpha_prev, po, stg[UO_OFF + ty * OWN_W + pos]);
+          a.rnew[go + c * g.nnx_pad] = ro[c];
+          a.pnew[go + c * g.nnx_pad] = vo[c];
+          a.u[go + c * g.nnx_pad] = fma(alpha_prev, pold_o[c], stg[UO_OFF + fuo + c * VB_W]);
 #endif
-            rz = fma(z, rn, rz);
-            rr = fma(rn, rn, rr);
-          }
+          rz = fma(N.pz[c], ro[c], rz);
+          rr = fma(ro[c], ro[c], rr);
         }
         acc[1] += rz;
         acc[2] += rr;
@@ -484,8 +480,8 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
       const unsigned mb = MKb[fmb];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        vb[c] = ((mb >> c) & 1u) ? 0.0 : stg[R_OFF + fvb + c];
-        N.pz[c] = stg[R_OFF + fvo + c];  // raw u (identity rows at fixed DOFs)
+        vb[c] = ((mb >> c) & 1u) ? 0.0 : stg[R_OFF + fvb + c * VB_W];
+        N.pz[c] = stg[R_OFF + fvo + c * VB_W];  // raw u (identity rows at fixed DOFs)
         vo[c] = ((N.pm >> c) & 1u) ? 0.0 : N.pz[c];
       }
     }
@@ -546,7 +542,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
     // (a segment's last NS steps issue nothing, so the next segment starts with free stages)
 
     if (it >= 2 && mine) {
-      const int gb = 3 * gi + rowd * gj + planed * (kn - 1);  // output node plane kn - 1
+      const int gb = g_own + planed * (kn - 1);  // output node plane kn - 1
       double pq = 0.0, zq = 0.0, qdq = 0.0;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -555,13 +551,13 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
         if (MODE == OP_PCG) {
           qv = fixed ? 0.0 : qv;
 #ifndef TOMO_EXP_NO_Q_STORE  // timing experiment only
-          a.out[gb + c] = qv;
+          a.out[gb + c * g.nnx_pad] = qv;
 #endif
           pq = fma(P.pv[c], qv, pq);
           zq = fma(P.pz[c], qv, zq);
           qdq = fma(P.pdi * qv, qv, qdq);
         } else {
-          a.out[gb + c] = fixed ? P.pz[c] : qv;
+          a.out[gb + c * g.nnx_pad] = fixed ? P.pz[c] : qv;
         }
       }
       acc[0] += pq;
@@ -606,6 +602,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
         s->pq = pq;
         s->rz = rz;
         s->rr = rr;
+        if (k < s->hist_n) s->hist[k] = rr;
 #ifdef TOMO_EXP_NOSTOP  // timing experiments: run exactly max_iters launches whatever the values
         if (k >= s->max_iters) { s->done = 2; s->iters = k; } else { s->alpha = 0.5; s->beta = 0.5; s->k = k + 1; }
         if (false) {
@@ -674,6 +671,7 @@ __global__ void k_scal_init(Scal* s, double tol_fnorm, int max_iters) {
   s->rr_true = 0.0; s->tol_fnorm = tol_fnorm; s->energy = 0.0; s->comp = 0.0;
   s->k = 0; s->iters = 0; s->done = 0; s->status = 0; s->max_iters = max_iters;
   s->domain_bad = 0; s->cntA = 0; s->cntB = 0; s->cntR = 0;
+  // hist / hist_n are set by the host (tomo_set_history) and kept across solves
 }
 
 // r = -q (padded), then r[load dof] += f (loads are distinct DOFs)
@@ -687,7 +685,7 @@ __global__ void k_add_loads(double* r, const int64_t* dofs, const double* vals, 
     r[dofs[i]] += vals[i];
 }
 
-// dense ABI vector -> padded internal vector, fixed entries zeroed
+// dense ABI vector (AoS) -> padded row-SoA internal vector, fixed entries zeroed
 __global__ void k_pack(Grid g, const double* __restrict__ dense, double* __restrict__ pad,
                        const uint8_t* __restrict__ mask) {
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -696,9 +694,8 @@ __global__ void k_pack(Grid g, const double* __restrict__ dense, double* __restr
     const int j = (int)((n / g.nnx) % g.nny);
     const int k = (int)(n / ((long long)g.nnx * g.nny));
     const unsigned m = mask ? mask[mask_index(g, i, j, k)] : 0u;  // NULL: no masking
-    const long long p = 3 * node_pad(g, i, j, k);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) pad[p + c] = ((m >> c) & 1u) ? 0.0 : dense[3 * n + c];
+    for (int c = 0; c < 3; ++c) pad[dof_pad(g, i, j, k, c)] = ((m >> c) & 1u) ? 0.0 : dense[3 * n + c];
   }
 }
 __global__ void k_unpack(Grid g, const double* __restrict__ pad, double* __restrict__ dense) {
@@ -707,9 +704,8 @@ __global__ void k_unpack(Grid g, const double* __restrict__ pad, double* __restr
     const int i = (int)(n % g.nnx);
     const int j = (int)((n / g.nnx) % g.nny);
     const int k = (int)(n / ((long long)g.nnx * g.nny));
-    const long long p = 3 * node_pad(g, i, j, k);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) dense[3 * n + c] = pad[p + c];
+    for (int c = 0; c < 3; ++c) dense[3 * n + c] = pad[dof_pad(g, i, j, k, c)];
   }
 }
 

@@ -33,12 +33,13 @@ __global__ void k_jacobi_smooth(Grid g, double omega, const double* __restrict__
   for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < g.nn; n += stride) {
     int i, j, k;
     node_of(g, n, i, j, k);
-    const long long p = 3 * node_pad(g, i, j, k);
     const unsigned m = mask[mask_index(g, i, j, k)];
     const double w = omega * dinv[node_pad(g, i, j, k)];
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-      x[p + c] = ((m >> c) & 1u) ? 0.0 : fma(w, b[p + c] - kx[p + c], x[p + c]);
+    for (int c = 0; c < 3; ++c) {
+      const long long p = dof_pad(g, i, j, k, c);
+      x[p] = ((m >> c) & 1u) ? 0.0 : fma(w, b[p] - kx[p], x[p]);
+    }
   }
 }
 
@@ -49,10 +50,12 @@ __global__ void k_residual(Grid g, const double* __restrict__ b, const double* _
   for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < g.nn; n += stride) {
     int i, j, k;
     node_of(g, n, i, j, k);
-    const long long p = 3 * node_pad(g, i, j, k);
     const unsigned m = mask[mask_index(g, i, j, k)];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) r[p + c] = ((m >> c) & 1u) ? 0.0 : b[p + c] - kx[p + c];
+    for (int c = 0; c < 3; ++c) {
+      const long long p = dof_pad(g, i, j, k, c);
+      r[p] = ((m >> c) & 1u) ? 0.0 : b[p] - kx[p];
+    }
   }
 }
 
@@ -81,16 +84,14 @@ __global__ void k_restrict(Grid gf, Grid gc, const double* __restrict__ rf,
           const int i = 2 * I + dx;
           if (i < 0 || i > gf.nx) continue;
           const double w = w1(i, I) * w1(j, J) * w1(k, K);
-          const long long p = 3 * node_pad(gf, i, j, k);
 #pragma unroll
-          for (int c = 0; c < 3; ++c) s[c] = fma(w, rf[p + c], s[c]);
+          for (int c = 0; c < 3; ++c) s[c] = fma(w, rf[dof_pad(gf, i, j, k, c)], s[c]);
         }
       }
     }
-    const long long q = 3 * node_pad(gc, I, J, K);
     const unsigned m = maskc[mask_index(gc, I, J, K)];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) rc[q + c] = ((m >> c) & 1u) ? 0.0 : s[c];
+    for (int c = 0; c < 3; ++c) rc[dof_pad(gc, I, J, K, c)] = ((m >> c) & 1u) ? 0.0 : s[c];
   }
 }
 
@@ -111,16 +112,17 @@ __global__ void k_prolong_add(Grid gf, Grid gc, const double* __restrict__ xc,
         for (int I = i >> 1; I <= (i + 1) >> 1; ++I) {
           if (I > gc.nx) continue;
           const double w = wy * w1(i, I);
-          const long long q = 3 * node_pad(gc, I, J, K);
 #pragma unroll
-          for (int c = 0; c < 3; ++c) s[c] = fma(w, xc[q + c], s[c]);
+          for (int c = 0; c < 3; ++c) s[c] = fma(w, xc[dof_pad(gc, I, J, K, c)], s[c]);
         }
       }
     }
-    const long long p = 3 * node_pad(gf, i, j, k);
     const unsigned m = maskf[mask_index(gf, i, j, k)];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) xf[p + c] = ((m >> c) & 1u) ? 0.0 : xf[p + c] + s[c];
+    for (int c = 0; c < 3; ++c) {
+      const long long p = dof_pad(gf, i, j, k, c);
+      xf[p] = ((m >> c) & 1u) ? 0.0 : xf[p] + s[c];
+    }
   }
 }
 

@@ -9,10 +9,12 @@
 namespace tomo {
 
 // Structured grid of nx*ny*nz hexahedra; (nx+1)(ny+1)(nz+1) nodes.
-// The ABI vectors are dense (node n = i + nnx(j + nny k)). The solver's internal vectors
-// use a PADDED layout: node rows of nnx_pad (even) nodes so that a row of 3-DOF nodes is a
-// multiple of 16 bytes (a TMA requirement); element fields use rows of nx_pad (even);
-// the per-node fixed mask uses byte rows of mp (multiple of 16).
+// The ABI vectors are dense AoS (DOF 3n+c, node n = i + nnx(j + nny k)). The solver's
+// internal vectors are PADDED ROW-SoA (dof_pad): a node row (j, k) is three component
+// sub-rows of nnx_pad (even) doubles, so every sub-row is a multiple of 16 bytes (a TMA
+// requirement) and a warp's 32 consecutive nodes of one component are 256 contiguous
+// bytes; element fields use rows of nx_pad (even); the per-node fixed mask uses byte rows
+// of mp (multiple of 16).
 struct Grid {
   int nx, ny, nz;     // elements per axis
   int nnx, nny, nnz;  // nodes per axis
@@ -23,6 +25,10 @@ struct Grid {
 
 __host__ __device__ inline long long node_pad(const Grid& g, int i, int j, int k) {
   return (long long)i + (long long)g.nnx_pad * (j + (long long)g.nny * k);
+}
+// internal (padded row-SoA) index of DOF c of node (i, j, k)
+__host__ __device__ inline long long dof_pad(const Grid& g, int i, int j, int k, int c) {
+  return (long long)i + (long long)g.nnx_pad * (c + 3 * (j + (long long)g.nny * k));
 }
 __host__ __device__ inline long long node_dense(const Grid& g, int i, int j, int k) {
   return (long long)i + (long long)g.nnx * (j + (long long)g.nny * k);
@@ -66,7 +72,8 @@ struct Scal {
   int max_iters;
   int domain_bad;     // a density outside [0,1] / NaN met by k_simp
   unsigned cntA, cntB, cntR;  // last-block counters (reset by the last block)
-  int pad;
+  int hist_n;         // length of hist (0: no residual history)
+  double* hist;       // optional device buffer: hist[k] = r_k^T r_k of launch k (tomo_set_history)
 };
 
 enum OpMode { OP_APPLY = 0, OP_PCG = 1 };
@@ -83,7 +90,8 @@ enum OpMode { OP_APPLY = 0, OP_PCG = 1 };
 #endif
 constexpr int OP_BY = TOMO_OP_BY;
 constexpr int OP_MINB = OP_BY >= 16 ? 1 : 2;  // resident blocks per SM the tile is sized for
-constexpr int OP_OX = 30;           // output nodes per tile along x (even: 16-B TMA rows)
+constexpr int OP_TX = 32;           // threads per tile row (lane tx <-> node / element column i0-1+tx)
+constexpr int OP_OX = 30;           // output nodes per tile along x
 constexpr int OP_OY = OP_BY - 1;    // output nodes per tile along y
 #ifndef TOMO_OP_NS
 #define TOMO_OP_NS 2

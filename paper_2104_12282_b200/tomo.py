@@ -93,6 +93,7 @@ _SIGS = [
     ("tomo_bench_dfma", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("tomo_set_profiling", C.c_int, [C.c_void_p, C.c_int]),
     ("tomo_set_graph", C.c_int, [C.c_void_p, C.c_int]),
+    ("tomo_set_history", C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     ("tomo_profile_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("tomo_bench_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_double)]),
     ("tomo_create_coarse", C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int]),
@@ -427,6 +428,13 @@ class Tomo:
     def set_graph(self, on: bool):
         """PCG loop as one CUDA graph (default) or host-batched launches (ncu-visible)."""
         self._check(self.lib.tomo_set_graph(self.h, 1 if on else 0))
+
+    def set_history(self, n: int):
+        """Record r_k^T r_k of every PCG launch of the next solves (n entries, device)."""
+        with torch.cuda.stream(self.stream):
+            self.hist = torch.zeros(max(n, 1), dtype=torch.float64, device=self.device)
+        self._check(self.lib.tomo_set_history(self.h, _ptr(self.hist) if n > 0 else None, n))
+        return self.hist
 
     def set_profiling(self, on: bool):
         self._check(self.lib.tomo_set_profiling(self.h, 1 if on else 0))

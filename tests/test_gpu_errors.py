@@ -75,7 +75,7 @@ def test_oc_nonfinite_inputs_are_enan(which, bad):
     rng = np.random.default_rng(1)
     x = rng.uniform(0.1, 0.9, p.n_elem)
     g = -rng.uniform(0, 1, p.n_elem)
-    arrs = {"x": x, "g": g, "dv": dv.copy()}
+    arrs = {"x": x.copy(), "g": g.copy(), "dv": dv.copy()}
     arrs[which][17] = bad
     with pytest.raises(ValueError):
         ooc.oc_update(arrs["x"], arrs["g"], arrs["dv"], P, 0.3)
