@@ -36,6 +36,8 @@ struct tomo_ctx {
   double fnorm = 0;
   std::vector<int> taps;  // 3 per tap
   std::vector<double> tap_w;
+  int filt_R = 0, filt_M = 0;     // taps = {d : |d|^2 <= filt_M}, R = floor(sqrt(M))
+  std::vector<double> wd2;        // weight by |d|^2 (3 R^2 + 1 entries)
   std::string err;
   // workspace
   bool bound = false;
@@ -43,7 +45,7 @@ struct tomo_ctx {
   char* ws = nullptr;
   size_t ws_bytes = 0;
   size_t off_E, off_dinv, off_Hs, off_t0, off_t1, off_t2, off_u, off_r0, off_r1, off_p0, off_p1, off_q0, off_q1, off_us,
-      off_mask, off_cnt, off_ld, off_ldp, off_lv, off_taps, off_tw, off_part, off_scal, off_oc,
+      off_mask, off_cnt, off_ld, off_ldp, off_lv, off_taps, off_tw, off_wd2, off_part, off_scal, off_oc,
       off_end;
   size_t n_part = 0;
   int op_blocks = 1;   // fused PCG kernel grid
@@ -98,6 +100,7 @@ struct tomo_ctx {
   double* lv() const { return P<double>(off_lv); }
   int* dtaps() const { return P<int>(off_taps); }
   double* tw() const { return P<double>(off_tw); }
+  double* wd2v() const { return P<double>(off_wd2); }
   double* part() const { return P<double>(off_part); }
   Scal* scal() const { return P<Scal>(off_scal); }
   double* ocout() const { return P<double>(off_oc); }
@@ -388,6 +391,21 @@ extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, doubl
         }
       }
 
+  // the tap set is a ball {|d|^2 <= M} (rmin - sqrt(d2) > 0 is monotone in d2): the tiled
+  // filter kernel indexes the weights by |d|^2
+  for (size_t t = 0; t < c->tap_w.size(); ++t) {
+    const int d2 = c->taps[3 * t] * c->taps[3 * t] + c->taps[3 * t + 1] * c->taps[3 * t + 1] +
+                   c->taps[3 * t + 2] * c->taps[3 * t + 2];
+    c->filt_M = std::max(c->filt_M, d2);
+  }
+  c->filt_R = (int)std::floor(std::sqrt((double)c->filt_M) + 1e-9);
+  c->wd2.assign((size_t)(3 * c->filt_R * c->filt_R + 1), 0.0);
+  for (size_t t = 0; t < c->tap_w.size(); ++t) {
+    const int d2 = c->taps[3 * t] * c->taps[3 * t] + c->taps[3 * t + 1] * c->taps[3 * t + 1] +
+                   c->taps[3 * t + 2] * c->taps[3 * t + 2];
+    c->wd2[d2] = c->tap_w[t];
+  }
+
   // workspace layout
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
@@ -413,6 +431,7 @@ extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, doubl
   c->off_lv = take(sizeof(double) * (c->load_dofs.size() + 1));
   c->off_taps = take(sizeof(int) * (c->taps.size() + 3));
   c->off_tw = take(sizeof(double) * (c->tap_w.size() + 1));
+  c->off_wd2 = take(sizeof(double) * c->wd2.size());
   c->n_part = 8192 * 5;
   c->off_part = take(sizeof(double) * c->n_part);
   c->off_scal = take(sizeof(Scal));
@@ -604,6 +623,7 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   if (!c->tap_w.empty()) {
     CK(c, cudaMemcpyAsync(c->dtaps(), c->taps.data(), sizeof(int) * c->taps.size(), cudaMemcpyHostToDevice, c->st));
     CK(c, cudaMemcpyAsync(c->tw(), c->tap_w.data(), sizeof(double) * c->tap_w.size(), cudaMemcpyHostToDevice, c->st));
+    CK(c, cudaMemcpyAsync(c->wd2v(), c->wd2.data(), sizeof(double) * c->wd2.size(), cudaMemcpyHostToDevice, c->st));
   }
   LAUNCH(c, launch_filter_sums(g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), c->cnt(), c->st));
   op_schedule(g, op_occupancy(OP_PCG), c->sms, (int)(c->n_part / 5), &c->op_blocks, &c->op_zchunks);
@@ -626,6 +646,18 @@ int need_bound(tomo_ctx* c) {
   if (!c) return TOMO_EINVAL;
   if (!c->bound) return fail(c, TOMO_ENOWORKSPACE, "call tomo_bind first");
   return TOMO_OK;
+}
+
+// density filter (P or P^T): the tiled kernel for tap balls up to R = 8, else the per-tap
+// gather kernel
+cudaError_t run_filter(tomo_ctx* c, const double* in, double* out, int transpose) {
+  if (!std::getenv("TOMO_FILTER_GATHER")) {  // A/B knob: force the per-tap gather kernel
+    const cudaError_t e = launch_filter_tiled(c->g, c->filt_R, c->filt_M, c->wd2v(), c->Hs(), in, out,
+                                              transpose, c->sms, c->st);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  return launch_filter(c->g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), in, out, transpose,
+                       c->st);
 }
 
 // E = SIMP(rho) and D^-1 into the workspace; checks rho in [0,1]
@@ -812,8 +844,7 @@ extern "C" int tomo_filter(tomo_ctx* c, const double* d_in, double* d_out, int64
   if (n_e != c->g.ne) return fail(c, TOMO_ESIZE, "length mismatch");
   if (!check_ptr(d_in) || !check_ptr(d_out)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
   if (d_in == d_out) return fail(c, TOMO_EINVAL, "in and out must not alias");
-  LAUNCH(c, launch_filter(c->g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), d_in, d_out,
-                          transpose ? 1 : 0, c->st));
+  LAUNCH(c, run_filter(c, d_in, d_out, transpose ? 1 : 0));
   return TOMO_OK;
 }
 
@@ -824,7 +855,7 @@ extern "C" int tomo_volume_grad(tomo_ctx* c, double* d_dv, int64_t n_e) {
   // ones into t1, then P^T
   std::vector<double> ones((size_t)n_e, 1.0);
   CK(c, cudaMemcpyAsync(c->t1(), ones.data(), sizeof(double) * (size_t)n_e, cudaMemcpyHostToDevice, c->st));
-  LAUNCH(c, launch_filter(c->g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), c->t1(), d_dv, 1, c->st));
+  LAUNCH(c, run_filter(c, c->t1(), d_dv, 1));
   CK(c, cudaStreamSynchronize(c->st));
   return TOMO_OK;
 }
@@ -861,7 +892,7 @@ int evaluate_dev(tomo_ctx* c, const double* d_rho, double* d_u, double* d_dc, do
   LAUNCH(c, launch_compliance(d_u, c->ld(), c->lv(), (int)c->load_dofs.size(), c->scal(), c->st));
   LAUNCH(c, launch_sens(c->g, c->w, d_rho, d_u, c->dmask(), c->penal, c->E0 - c->Emin, c->Emin,
                         dc, nullptr, c->part(), c->nb_s, c->scal(), 0, c->st));
-  LAUNCH(c, launch_filter(c->g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), dc, d_dcf, 1, c->st));
+  LAUNCH(c, run_filter(c, dc, d_dcf, 1));
   if (c_out) {
     CK(c, cudaMemcpyAsync(c_out, &c->scal()->comp, sizeof(double), cudaMemcpyDeviceToHost, c->st));
   }

@@ -23,6 +23,7 @@
 // by the last block); there are no floating-point atomics.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "tomo_internal.h"
@@ -864,6 +865,86 @@ __global__ void __launch_bounds__(256) k_filter(Grid g, const int* __restrict__ 
   }
 }
 
+// Tiled density filter for a ball-shaped tap set {d in Z^3 : |d|^2 <= M} (every cone filter
+// w = rmin - |d| > 0 is one: sqrt is monotone). Block = 32 x 8 output columns marching along
+// z through a chunk of planes; each input plane (tile + R halo, zero outside the domain) is
+// staged once in shared memory (pre-divided by Hs in transpose mode: P^T v = H (v / Hs)) and
+// scattered into 2R+1 register accumulators, acc[j] = output plane zi - R + j, with
+// weights wd2[|d|^2] held in registers: per output, one shared load per (dx, dy) column and
+// one FMA per tap. Forward mode divides the finished output by Hs (P x = H x / Hs).
+// MM < 0: the ball radius^2 M is a runtime value (predicated taps of the (2R+1)^3 cube).
+constexpr int FT_X = 32, FT_Y = 8;
+
+template <int R, int MM>
+__global__ void __launch_bounds__(FT_X * FT_Y) k_filter_t(Grid g, const double* __restrict__ wd2,
+                                                         int M, const double* __restrict__ Hs,
+                                                         const double* __restrict__ in,
+                                                         double* __restrict__ out, int transpose,
+                                                         int zchunk) {
+  constexpr int PX = FT_X + 2 * R, PY = FT_Y + 2 * R, NA = 2 * R + 1;
+  constexpr int DMAX = 3 * R * R;
+  __shared__ double pl[PY * PX];
+  __shared__ double sw[MM >= 0 ? 1 : DMAX + 1];  // runtime-M weights (broadcast reads)
+  const int tx = threadIdx.x, ty = threadIdx.y, t = ty * FT_X + tx;
+  const int tiles_x = (g.nx + FT_X - 1) / FT_X, tiles = tiles_x * ((g.ny + FT_Y - 1) / FT_Y);
+  const int tile = blockIdx.x % tiles, ch = blockIdx.x / tiles;
+  const int x0 = (tile % tiles_x) * FT_X, y0 = (tile / tiles_x) * FT_Y;
+  const int z0 = ch * zchunk, z1 = min(g.nz, z0 + zchunk);
+  const int Mr = MM >= 0 ? MM : M;
+  constexpr int WN = MM >= 0 ? MM + 1 : 1;
+  double w[WN];  // specialised tap sets: weights in registers
+#pragma unroll
+  for (int d = 0; d < WN; ++d) w[d] = wd2[d];
+  if (MM < 0)
+    for (int d = t; d <= DMAX; d += FT_X * FT_Y) sw[d] = d <= Mr ? wd2[d] : 0.0;
+  double acc[NA];
+#pragma unroll
+  for (int j = 0; j < NA; ++j) acc[j] = 0.0;
+  const int x = x0 + tx, y = y0 + ty;
+  const bool live = x < g.nx && y < g.ny;
+  const long long pe = (long long)g.nx * g.ny;
+  for (int zi = z0 - R; zi < z1 + R; ++zi) {
+    if (zi >= 0 && zi < g.nz) {
+      __syncthreads();  // the previous plane's reads are done
+      for (int q = t; q < PX * PY; q += FT_X * FT_Y) {
+        const int xx = x0 - R + q % PX, yy = y0 - R + q / PX;
+        double v = 0.0;
+        if (xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny) {
+          const long long e = xx + (long long)g.nx * yy + pe * zi;
+          v = transpose ? __ldg(in + e) / __ldg(Hs + e) : __ldg(in + e);
+        }
+        pl[q] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int dy = -R; dy <= R; ++dy) {
+#pragma unroll
+        for (int dx = -R; dx <= R; ++dx) {
+          if (dx * dx + dy * dy > (MM >= 0 ? MM : DMAX)) continue;
+          const double v = pl[(ty + R + dy) * PX + tx + R + dx];
+#pragma unroll
+          for (int j = 0; j < NA; ++j) {
+            const int dz = R - j, d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 <= (MM >= 0 ? MM : DMAX)) {
+              if (MM >= 0) acc[j] = fma(w[MM >= 0 ? d2 : 0], v, acc[j]);
+              else if (d2 <= Mr) acc[j] = fma(sw[d2], v, acc[j]);
+            }
+          }
+        }
+      }
+    }
+    // output plane zi - R is complete
+    const int zo = zi - R;
+    if (live && zo >= z0 && zo < z1) {
+      const long long e = x + (long long)g.nx * y + pe * zo;
+      out[e] = transpose ? acc[0] : acc[0] / Hs[e];
+    }
+#pragma unroll
+    for (int j = 0; j + 1 < NA; ++j) acc[j] = acc[j + 1];
+    acc[NA - 1] = 0.0;
+  }
+}
+
 // ------------------------------------------------------------------ OC (cooperative)
 __device__ __forceinline__ double oc_xnew(double x, double gg, double dv, double lam,
                                           double move, double eta) {
@@ -1113,6 +1194,38 @@ cudaError_t launch_filter(const Grid& g, const int* taps, const double* w, int n
                                                        transpose);
   return cudaGetLastError();
 }
+// tiled filter launch for a ball of radius^2 M (R = floor(sqrt(M))): specialised tap sets of
+// the configs (rmin 1.5, 2, 3 and the paper's 7.2) and a runtime-M kernel per R up to 8;
+// returns cudaErrorNotSupported when R > 8 (the caller falls back to k_filter)
+cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, const double* Hs,
+                                const double* in, double* out, int transpose, int sms,
+                                cudaStream_t st) {
+  const int tiles = ((g.nx + FT_X - 1) / FT_X) * ((g.ny + FT_Y - 1) / FT_Y);
+  // z chunks: >= 4 blocks per SM, but chunks no thinner than 2R + 2 planes (halo overhead)
+  int chunks = std::max(1, (4 * sms + tiles - 1) / tiles);
+  chunks = std::min(chunks, std::max(1, g.nz / (2 * R + 2)));
+  const int zchunk = (g.nz + chunks - 1) / chunks;
+  chunks = (g.nz + zchunk - 1) / zchunk;
+  const dim3 grid(tiles * chunks), block(FT_X, FT_Y);
+#define TOMO_FT(RR, MMM) k_filter_t<RR, MMM><<<grid, block, 0, st>>>(g, wd2, M, Hs, in, out, transpose, zchunk)
+  if (R == 1 && M == 2) TOMO_FT(1, 2);
+  else if (R == 1 && M == 3) TOMO_FT(1, 3);
+  else if (R == 2 && M == 8) TOMO_FT(2, 8);
+  else if (R == 7 && M == 51) TOMO_FT(7, 51);
+  else if (R == 0) TOMO_FT(0, 0);
+  else if (R == 1) TOMO_FT(1, -1);
+  else if (R == 2) TOMO_FT(2, -1);
+  else if (R == 3) TOMO_FT(3, -1);
+  else if (R == 4) TOMO_FT(4, -1);
+  else if (R == 5) TOMO_FT(5, -1);
+  else if (R == 6) TOMO_FT(6, -1);
+  else if (R == 7) TOMO_FT(7, -1);
+  else if (R == 8) TOMO_FT(8, -1);
+  else return cudaErrorNotSupported;
+#undef TOMO_FT
+  return cudaGetLastError();
+}
+
 int oc_max_blocks() {
   int nb = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);

@@ -165,7 +165,14 @@ def test_tiny_cantilever_golden():
 
 # ------------------------------------------------------------------ filter, OC
 @pytest.mark.parametrize("nx,ny,nz,rmin", [(24, 12, 12, 1.5), (9, 5, 4, 2.0), (13, 7, 8, 3.0),
-                                           (1, 1, 1, 1.5), (4, 3, 2, 0.9)])
+                                           (1, 1, 1, 1.5), (4, 3, 2, 0.9),
+                                           # tiled kernel: every specialised / runtime-radius
+                                           # path, ragged tiles (32 x 8) and several z chunks
+                                           (70, 19, 37, 3.0), (45, 17, 29, 1.5), (33, 9, 40, 2.0),
+                                           (37, 11, 23, 1.8), (35, 10, 26, 2.5), (29, 13, 31, 3.7),
+                                           (26, 12, 30, 4.5), (27, 11, 33, 5.5), (25, 10, 28, 6.5),
+                                           (40, 18, 35, 7.2), (21, 12, 25, 8.5), (20, 11, 22, 9.5),
+                                           (5, 40, 3, 3.0)])
 def test_filter_parity(nx, ny, nz, rmin):
     p = inputs.Problem("f", nx, ny, nz, rmin=rmin)
     t = ctx_for(p)
@@ -192,7 +199,7 @@ def test_oc_parity_1000_random_instances():
     dv_g = t.volume_grad()
     assert rel(cpu(dv_g), dv) <= 1e-14
     n = nx * ny * nz
-    flips = unreachable = 0
+    flips = unreachable = wide = 0
     for inst in range(1000):
         x = rng.uniform(0.0, 1.0, n)
         g = -rng.uniform(0, 1, n) ** 3 * 10 ** rng.uniform(-3, 3)
@@ -210,15 +217,22 @@ def test_oc_parity_1000_random_instances():
             assert abs(float(np.sum(P @ xh)) - vf * n) <= 1e-6 * vf * n
         else:
             unreachable += 1
-        assert abs(lam - lam_ref) <= 1e-13 * lam_ref
         assert np.max(np.abs(xh - xn_ref)) <= 1e-12
         if lam != lam_ref:
             flips += 1
+            # a flip is admissible only where the volume decision is at rounding level: the
+            # oracle's own volume at the GPU's lambda meets the target to 1e-12. Where V(lambda)
+            # is flat there (every element at a move limit) lambda itself is ill-determined
+            # while x is not, so lambda is compared only when the volume is not flat.
             v_at = float(np.sum(P @ ooc.x_new(x, g, dv, lam, move, 0.5)))
             assert abs(v_at - vf * n) <= 1e-12 * vf * n, (inst, v_at, vf * n)
-    print(f"OC 1000 instances: {flips} lambda flips (all at rounding-level volume decisions), "
-          f"{unreachable} unreachable targets")
-    assert flips <= 500
+            if abs(lam - lam_ref) > 1e-13 * lam_ref:
+                wide += 1
+                v_ref_at = float(np.sum(P @ ooc.x_new(x, g, dv, lam_ref, move, 0.5)))
+                assert abs(v_at - v_ref_at) <= 1e-12 * vf * n, (inst, lam, lam_ref)
+    print(f"OC 1000 instances: {flips} lambda flips (all at rounding-level volume decisions; "
+          f"{wide} on a flat V(lambda)), {unreachable} unreachable targets")
+    assert flips <= 500 and wide <= 50
 
 
 # ------------------------------------------------------------------ edges and errors
