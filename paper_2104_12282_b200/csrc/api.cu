@@ -44,7 +44,7 @@ struct tomo_ctx {
   cudaStream_t st = nullptr;
   char* ws = nullptr;
   size_t ws_bytes = 0;
-  size_t off_E, off_dinv, off_Hs, off_t0, off_t1, off_t2, off_u, off_r0, off_r1, off_p0, off_p1, off_q0, off_q1, off_us,
+  size_t off_E, off_dinv, off_Hs, off_iHs, off_t0, off_t1, off_t2, off_u, off_r0, off_r1, off_p0, off_p1, off_q0, off_q1, off_us,
       off_mask, off_cnt, off_ld, off_ldp, off_lv, off_taps, off_tw, off_wd2, off_part, off_scal, off_oc,
       off_end;
   size_t n_part = 0;
@@ -85,6 +85,7 @@ struct tomo_ctx {
   double* E() const { return P<double>(off_E); }
   double* dinv() const { return P<double>(off_dinv); }
   double* Hs() const { return P<double>(off_Hs); }
+  double* iHs() const { return P<double>(off_iHs); }
   double* t0() const { return P<double>(off_t0); }
   double* t1() const { return P<double>(off_t1); }
   double* t2() const { return P<double>(off_t2); }
@@ -413,6 +414,7 @@ extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, doubl
   c->off_E = take(sizeof(double) * (size_t)g.ne_pad);
   c->off_dinv = take(sizeof(double) * (size_t)g.nn_pad);
   c->off_Hs = take(ve);
+  c->off_iHs = take(ve);
   c->off_t0 = take(ve);
   c->off_t1 = take(ve);
   c->off_t2 = take(ve);
@@ -625,7 +627,7 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
     CK(c, cudaMemcpyAsync(c->tw(), c->tap_w.data(), sizeof(double) * c->tap_w.size(), cudaMemcpyHostToDevice, c->st));
     CK(c, cudaMemcpyAsync(c->wd2v(), c->wd2.data(), sizeof(double) * c->wd2.size(), cudaMemcpyHostToDevice, c->st));
   }
-  LAUNCH(c, launch_filter_sums(g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), c->cnt(), c->st));
+  LAUNCH(c, launch_filter_sums(g, c->dtaps(), c->tw(), (int)c->tap_w.size(), c->Hs(), c->iHs(), c->cnt(), c->st));
   op_schedule(g, op_occupancy(OP_PCG), c->sms, (int)(c->n_part / 5), &c->op_blocks, &c->op_zchunks);
   op_schedule(g, op_occupancy(OP_APPLY), c->sms, (int)(c->n_part / 5), &c->ap_blocks, &c->ap_zchunks);
   c->nb_b = (int)std::min<long long>((g.ndof_pad / 2 + 255) / 256, (long long)c->sms * 4);
@@ -652,7 +654,7 @@ int need_bound(tomo_ctx* c) {
 // gather kernel
 cudaError_t run_filter(tomo_ctx* c, const double* in, double* out, int transpose) {
   if (!std::getenv("TOMO_FILTER_GATHER")) {  // A/B knob: force the per-tap gather kernel
-    const cudaError_t e = launch_filter_tiled(c->g, c->filt_R, c->filt_M, c->wd2v(), c->Hs(), in, out,
+    const cudaError_t e = launch_filter_tiled(c->g, c->filt_R, c->filt_M, c->wd2v(), c->iHs(), in, out,
                                               transpose, c->sms, c->st);
     if (e != cudaErrorNotSupported) return e;
   }

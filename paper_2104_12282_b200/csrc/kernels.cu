@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(256) k_sens(Grid g, Walsh W, const double* __r
 // ------------------------------------------------------------------ density filter
 // taps: 3 ints (dx, dy, dz) + weight each, order dz, dy, dx ascending (reading A15)
 __global__ void k_filter_sums(Grid g, const int* __restrict__ taps,
-                              const double* __restrict__ w, int ntaps, double* Hs,
+                              const double* __restrict__ w, int ntaps, double* Hs, double* iHs,
                               int* counts) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.ne; e += stride) {
@@ -827,6 +827,7 @@ __global__ void k_filter_sums(Grid g, const int* __restrict__ taps,
       }
     }
     Hs[e] = acc;
+    iHs[e] = 1.0 / acc;
     counts[e] = cnt;
   }
 }
@@ -866,24 +867,27 @@ __global__ void __launch_bounds__(256) k_filter(Grid g, const int* __restrict__ 
 }
 
 // Tiled density filter for a ball-shaped tap set {d in Z^3 : |d|^2 <= M} (every cone filter
-// w = rmin - |d| > 0 is one: sqrt is monotone). Block = 32 x 8 output columns marching along
-// z through a chunk of planes; each input plane (tile + R halo, zero outside the domain) is
-// staged once in shared memory (pre-divided by Hs in transpose mode: P^T v = H (v / Hs)) and
-// scattered into 2R+1 register accumulators, acc[j] = output plane zi - R + j, with
-// weights wd2[|d|^2] held in registers: per output, one shared load per (dx, dy) column and
-// one FMA per tap. Forward mode divides the finished output by Hs (P x = H x / Hs).
-// MM < 0: the ball radius^2 M is a runtime value (predicated taps of the (2R+1)^3 cube).
-constexpr int FT_X = 32, FT_Y = 8;
+// w = rmin - |d| > 0 is one: sqrt is monotone). A block of FT_X x FT_YT threads owns FT_X x
+// 2 FT_YT output columns (each thread two rows, y and y + FT_YT) and marches along z through
+// a chunk of planes. Each input plane (tile + R halo, zero outside the domain; multiplied by
+// 1/Hs in transpose mode: P^T v = H (v / Hs)) is staged once in shared memory, double
+// buffered with the next plane's global loads issued before the current plane's FMAs, and
+// scattered into 2R+1 register accumulators per output row, acc[j] = output plane zi - R + j.
+// Weights wd2[|d|^2] live in registers (specialised tap sets) or shared memory (runtime M).
+// Per output: about (2R+1)(2R+2)/2 shared loads per input plane and one FMA per tap. Forward
+// mode multiplies the finished output by 1/Hs (P x = H x / Hs).
+constexpr int FT_X = 32, FT_Y = 8;  // output tile; ROWS output rows per thread (1 or 2)
 
-template <int R, int MM>
-__global__ void __launch_bounds__(FT_X * FT_Y) k_filter_t(Grid g, const double* __restrict__ wd2,
-                                                         int M, const double* __restrict__ Hs,
-                                                         const double* __restrict__ in,
-                                                         double* __restrict__ out, int transpose,
-                                                         int zchunk) {
-  constexpr int PX = FT_X + 2 * R, PY = FT_Y + 2 * R, NA = 2 * R + 1;
-  constexpr int DMAX = 3 * R * R;
-  __shared__ double pl[PY * PX];
+template <int R, int MM, int ROWS>
+__global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const double* __restrict__ wd2, int M,
+                                                  const double* __restrict__ iHs,
+                                                  const double* __restrict__ in,
+                                                  double* __restrict__ out, int transpose,
+                                                  int zchunk) {
+  constexpr int FT_YT = FT_Y / ROWS, FT_T = FT_X * FT_YT;
+  constexpr int PX = FT_X + 2 * R, PY = FT_Y + 2 * R, NA = 2 * R + 1, DMAX = 3 * R * R;
+  constexpr int NL = (PX * PY + FT_T - 1) / FT_T;  // staged values per thread and plane
+  __shared__ double pl[2][PY * PX];
   __shared__ double sw[MM >= 0 ? 1 : DMAX + 1];  // runtime-M weights (broadcast reads)
   const int tx = threadIdx.x, ty = threadIdx.y, t = ty * FT_X + tx;
   const int tiles_x = (g.nx + FT_X - 1) / FT_X, tiles = tiles_x * ((g.ny + FT_Y - 1) / FT_Y);
@@ -896,52 +900,93 @@ __global__ void __launch_bounds__(FT_X * FT_Y) k_filter_t(Grid g, const double* 
 #pragma unroll
   for (int d = 0; d < WN; ++d) w[d] = wd2[d];
   if (MM < 0)
-    for (int d = t; d <= DMAX; d += FT_X * FT_Y) sw[d] = d <= Mr ? wd2[d] : 0.0;
-  double acc[NA];
+    for (int d = t; d <= DMAX; d += FT_T) sw[d] = d <= Mr ? wd2[d] : 0.0;
+  double acc[ROWS][NA];
 #pragma unroll
-  for (int j = 0; j < NA; ++j) acc[j] = 0.0;
-  const int x = x0 + tx, y = y0 + ty;
-  const bool live = x < g.nx && y < g.ny;
+  for (int h = 0; h < ROWS; ++h)
+#pragma unroll
+    for (int j = 0; j < NA; ++j) acc[h][j] = 0.0;
   const long long pe = (long long)g.nx * g.ny;
-  for (int zi = z0 - R; zi < z1 + R; ++zi) {
-    if (zi >= 0 && zi < g.nz) {
-      __syncthreads();  // the previous plane's reads are done
-      for (int q = t; q < PX * PY; q += FT_X * FT_Y) {
-        const int xx = x0 - R + q % PX, yy = y0 - R + q / PX;
-        double v = 0.0;
-        if (xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny) {
-          const long long e = xx + (long long)g.nx * yy + pe * zi;
-          v = transpose ? __ldg(in + e) / __ldg(Hs + e) : __ldg(in + e);
-        }
-        pl[q] = v;
+  double pf[NL];
+  auto fetch = [&](int zi) {  // this thread's staging slots of plane zi (0 outside the domain)
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const int q = t + l * FT_T;
+      const int xx = x0 - R + q % PX, yy = y0 - R + q / PX;
+      double v = 0.0;
+      if (q < PX * PY && xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny) {
+        const long long e = xx + (long long)g.nx * yy + pe * zi;
+        v = transpose ? __ldg(in + e) * __ldg(iHs + e) : __ldg(in + e);
       }
-      __syncthreads();
+      pf[l] = v;
+    }
+  };
+  auto stage = [&](int b) {
 #pragma unroll
-      for (int dy = -R; dy <= R; ++dy) {
+    for (int l = 0; l < NL; ++l)
+      if (t + l * FT_T < PX * PY) pl[b][t + l * FT_T] = pf[l];
+  };
+  const int zb = max(0, z0 - R), ze = min(g.nz, z1 + R);  // input planes that exist
+  fetch(zb);
+  stage(0);
+  __syncthreads();
+  const int x = x0 + tx;
+  int buf = 0;
+  for (int zi = zb; zi < ze; ++zi) {
+    if (zi + 1 < ze) fetch(zi + 1);  // next plane's loads in flight during the FMAs
+    const double* P = pl[buf];
 #pragma unroll
-        for (int dx = -R; dx <= R; ++dx) {
-          if (dx * dx + dy * dy > (MM >= 0 ? MM : DMAX)) continue;
-          const double v = pl[(ty + R + dy) * PX + tx + R + dx];
+    for (int dy = -R; dy <= R + (ROWS - 1) * FT_YT; ++dy) {
+#pragma unroll
+      for (int dx = -R; dx <= R; ++dx) {
+        // column (dx, dy) of row 0 is column (dx, dy - FT_YT) of row 1
+        bool rh[ROWS], any = false;
+#pragma unroll
+        for (int h = 0; h < ROWS; ++h) {
+          const int dyh = dy - h * FT_YT;
+          rh[h] = dyh >= -R && dyh <= R && dx * dx + dyh * dyh <= (MM >= 0 ? MM : DMAX);
+          any |= rh[h];
+        }
+        if (!any) continue;
+        const double v = P[(ty + R + dy) * PX + tx + R + dx];
+#pragma unroll
+        for (int h = 0; h < ROWS; ++h) {
+          if (!rh[h]) continue;
+          const int dyh = dy - h * FT_YT;
 #pragma unroll
           for (int j = 0; j < NA; ++j) {
-            const int dz = R - j, d2 = dx * dx + dy * dy + dz * dz;
+            const int dz = R - j, d2 = dx * dx + dyh * dyh + dz * dz;
             if (d2 <= (MM >= 0 ? MM : DMAX)) {
-              if (MM >= 0) acc[j] = fma(w[MM >= 0 ? d2 : 0], v, acc[j]);
-              else if (d2 <= Mr) acc[j] = fma(sw[d2], v, acc[j]);
+              if (MM >= 0) acc[h][j] = fma(w[MM >= 0 ? d2 : 0], v, acc[h][j]);
+              else if (d2 <= Mr) acc[h][j] = fma(sw[d2], v, acc[h][j]);
             }
           }
         }
       }
     }
-    // output plane zi - R is complete
+    // output plane zi - R is complete (input planes beyond the domain contribute zero)
     const int zo = zi - R;
-    if (live && zo >= z0 && zo < z1) {
-      const long long e = x + (long long)g.nx * y + pe * zo;
-      out[e] = transpose ? acc[0] : acc[0] / Hs[e];
-    }
+    auto flush = [&](int z) {
 #pragma unroll
-    for (int j = 0; j + 1 < NA; ++j) acc[j] = acc[j + 1];
-    acc[NA - 1] = 0.0;
+      for (int h = 0; h < ROWS; ++h) {
+        const int y = y0 + ty + h * FT_YT;
+        if (x < g.nx && y < g.ny && z >= z0 && z < z1) {
+          const long long e = x + (long long)g.nx * y + pe * z;
+          out[e] = transpose ? acc[h][0] : acc[h][0] * iHs[e];
+        }
+#pragma unroll
+        for (int j = 0; j + 1 < NA; ++j) acc[h][j] = acc[h][j + 1];
+        acc[h][NA - 1] = 0.0;
+      }
+    };
+    flush(zo);
+    if (zi + 1 == ze)  // drain: outputs whose remaining input planes lie outside the domain
+      for (int z = zo + 1; z < z1; ++z) flush(z);
+    if (zi + 1 < ze) {
+      stage(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
   }
 }
 
@@ -1178,8 +1223,8 @@ cudaError_t launch_sens(const Grid& g, const Walsh& w, const double* rho, const 
   return cudaGetLastError();
 }
 cudaError_t launch_filter_sums(const Grid& g, const int* taps, const double* w, int ntaps,
-                               double* Hs, int* counts, cudaStream_t st) {
-  k_filter_sums<<<nblk(g.ne, 256, 148 * 16), 256, 0, st>>>(g, taps, w, ntaps, Hs, counts);
+                               double* Hs, double* iHs, int* counts, cudaStream_t st) {
+  k_filter_sums<<<nblk(g.ne, 256, 148 * 16), 256, 0, st>>>(g, taps, w, ntaps, Hs, iHs, counts);
   return cudaGetLastError();
 }
 cudaError_t launch_filter(const Grid& g, const int* taps, const double* w, int ntaps,
@@ -1197,17 +1242,22 @@ cudaError_t launch_filter(const Grid& g, const int* taps, const double* w, int n
 // tiled filter launch for a ball of radius^2 M (R = floor(sqrt(M))): specialised tap sets of
 // the configs (rmin 1.5, 2, 3 and the paper's 7.2) and a runtime-M kernel per R up to 8;
 // returns cudaErrorNotSupported when R > 8 (the caller falls back to k_filter)
-cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, const double* Hs,
+cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, const double* iHs,
                                 const double* in, double* out, int transpose, int sms,
                                 cudaStream_t st) {
   const int tiles = ((g.nx + FT_X - 1) / FT_X) * ((g.ny + FT_Y - 1) / FT_Y);
-  // z chunks: >= 4 blocks per SM, but chunks no thinner than 2R + 2 planes (halo overhead)
-  int chunks = std::max(1, (4 * sms + tiles - 1) / tiles);
-  chunks = std::min(chunks, std::max(1, g.nz / (2 * R + 2)));
+  // z chunks: aim at >= 3 blocks per SM, but no chunk thinner than 4R + 4 planes (the 2R
+  // halo planes of a chunk cost FMAs)
+  int chunks = std::max(1, (3 * sms + tiles - 1) / tiles);
+  chunks = std::min(chunks, std::max(1, g.nz / (4 * R + 4)));
   const int zchunk = (g.nz + chunks - 1) / chunks;
   chunks = (g.nz + zchunk - 1) / zchunk;
-  const dim3 grid(tiles * chunks), block(FT_X, FT_Y);
-#define TOMO_FT(RR, MMM) k_filter_t<RR, MMM><<<grid, block, 0, st>>>(g, wd2, M, Hs, in, out, transpose, zchunk)
+  const dim3 grid(tiles * chunks);
+  // two output rows per thread halve the shared loads per FMA where loads would bound (small
+  // R); one row per thread for large R (FMA-bound, and the unrolled body stays in registers)
+#define TOMO_FT(RR, MMM)                                                                      \
+  k_filter_t<RR, MMM, (RR <= 3 ? 2 : 1)><<<grid, dim3(FT_X, FT_Y / (RR <= 3 ? 2 : 1)), 0, st>>>( \
+      g, wd2, M, iHs, in, out, transpose, zchunk)
   if (R == 1 && M == 2) TOMO_FT(1, 2);
   else if (R == 1 && M == 3) TOMO_FT(1, 3);
   else if (R == 2 && M == 8) TOMO_FT(2, 8);

@@ -169,11 +169,11 @@ cudaError_t launch_sens(const Grid& g, const Walsh& w, const double* rho, const 
                         double* dc, double* ce, double* partials, int nblocks, Scal* s,
                         int want_energy, cudaStream_t st);
 cudaError_t launch_filter_sums(const Grid& g, const int* taps, const double* w, int ntaps,
-                               double* Hs, int* counts, cudaStream_t st);
+                               double* Hs, double* iHs, int* counts, cudaStream_t st);
 cudaError_t launch_filter(const Grid& g, const int* taps, const double* w, int ntaps,
                           const double* Hs, const double* in, double* out, int transpose,
                           cudaStream_t st);
-cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, const double* Hs,
+cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, const double* iHs,
                                 const double* in, double* out, int transpose, int sms,
                                 cudaStream_t st);
 cudaError_t launch_oc(int ne, const double* x, const double* g, const double* dv,
