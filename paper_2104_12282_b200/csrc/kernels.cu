@@ -907,34 +907,45 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const d
 #pragma unroll
     for (int j = 0; j < NA; ++j) acc[h][j] = 0.0;
   const long long pe = (long long)g.nx * g.ny;
-  double pf[NL];
-  auto fetch = [&](int zi) {  // this thread's staging slots of plane zi (0 outside the domain)
+  auto fetch = [&](double (&pf)[NL], int zi) {  // this thread's staging slots of plane zi
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       const int q = t + l * FT_T;
       const int xx = x0 - R + q % PX, yy = y0 - R + q / PX;
       double v = 0.0;
-      if (q < PX * PY && xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny) {
+      if (q < PX * PY && xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zi < g.nz) {
         const long long e = xx + (long long)g.nx * yy + pe * zi;
         v = transpose ? __ldg(in + e) * __ldg(iHs + e) : __ldg(in + e);
       }
       pf[l] = v;
     }
   };
-  auto stage = [&](int b) {
+  auto stage = [&](int b, const double (&pf)[NL]) {
 #pragma unroll
     for (int l = 0; l < NL; ++l)
       if (t + l * FT_T < PX * PY) pl[b][t + l * FT_T] = pf[l];
   };
   const int zb = max(0, z0 - R), ze = min(g.nz, z1 + R);  // input planes that exist
-  fetch(zb);
-  stage(0);
-  __syncthreads();
   const int x = x0 + tx;
-  int buf = 0;
-  for (int zi = zb; zi < ze; ++zi) {
-    if (zi + 1 < ze) fetch(zi + 1);  // next plane's loads in flight during the FMAs
-    const double* P = pl[buf];
+  // output plane z is complete once input plane z + R is in (or the domain ends)
+  auto flush = [&](int z) {
+#pragma unroll
+    for (int h = 0; h < ROWS; ++h) {
+      const int y = y0 + ty + h * FT_YT;
+      if (x < g.nx && y < g.ny && z >= z0 && z < z1) {
+        const long long e = x + (long long)g.nx * y + pe * z;
+        out[e] = transpose ? acc[h][0] : acc[h][0] * iHs[e];
+      }
+#pragma unroll
+      for (int j = 0; j + 1 < NA; ++j) acc[h][j] = acc[h][j + 1];
+      acc[h][NA - 1] = 0.0;
+    }
+  };
+  // input plane zi from smem buffer b; the loads of plane zi + 2 go to F while the FMAs run,
+  // plane zi + 1 (fetched one step earlier into S) is staged into the other buffer at the end
+  auto step = [&](int zi, int b, double (&F)[NL], const double (&S)[NL]) {
+    if (zi + 2 < ze) fetch(F, zi + 2);
+    const double* P = pl[b];
 #pragma unroll
     for (int dy = -R; dy <= R + (ROWS - 1) * FT_YT; ++dy) {
 #pragma unroll
@@ -964,29 +975,22 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const d
         }
       }
     }
-    // output plane zi - R is complete (input planes beyond the domain contribute zero)
-    const int zo = zi - R;
-    auto flush = [&](int z) {
-#pragma unroll
-      for (int h = 0; h < ROWS; ++h) {
-        const int y = y0 + ty + h * FT_YT;
-        if (x < g.nx && y < g.ny && z >= z0 && z < z1) {
-          const long long e = x + (long long)g.nx * y + pe * z;
-          out[e] = transpose ? acc[h][0] : acc[h][0] * iHs[e];
-        }
-#pragma unroll
-        for (int j = 0; j + 1 < NA; ++j) acc[h][j] = acc[h][j + 1];
-        acc[h][NA - 1] = 0.0;
-      }
-    };
-    flush(zo);
+    flush(zi - R);
     if (zi + 1 == ze)  // drain: outputs whose remaining input planes lie outside the domain
-      for (int z = zo + 1; z < z1; ++z) flush(z);
+      for (int z = zi - R + 1; z < z1; ++z) flush(z);
     if (zi + 1 < ze) {
-      stage(buf ^ 1);
+      stage(b ^ 1, S);
       __syncthreads();
-      buf ^= 1;
     }
+  };
+  double pa[NL], pb[NL];
+  fetch(pa, zb);
+  fetch(pb, zb + 1);
+  stage(0, pa);
+  __syncthreads();
+  for (int zi = zb; zi < ze; zi += 2) {
+    step(zi, 0, pa, pb);
+    if (zi + 1 < ze) step(zi + 1, 1, pb, pa);
   }
 }
 
