@@ -907,44 +907,60 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const d
 #pragma unroll
     for (int j = 0; j < NA; ++j) acc[h][j] = 0.0;
   const long long pe = (long long)g.nx * g.ny;
-  auto fetch = [&](double (&pf)[NL], int zi) {  // this thread's staging slots of plane zi
+  // raw loads only (the transpose scaling by 1/Hs happens at staging time), so that the
+  // loads stay in flight while the FMAs of the current plane run
+  struct Pf { double a[NL], b[NL]; };
+  auto fetch = [&](Pf& pf, int zi) {  // this thread's staging slots of plane zi
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       const int q = t + l * FT_T;
       const int xx = x0 - R + q % PX, yy = y0 - R + q / PX;
-      double v = 0.0;
+      double va = 0.0, vb = 0.0;
       if (q < PX * PY && xx >= 0 && xx < g.nx && yy >= 0 && yy < g.ny && zi < g.nz) {
         const long long e = xx + (long long)g.nx * yy + pe * zi;
-        v = transpose ? __ldg(in + e) * __ldg(iHs + e) : __ldg(in + e);
+        va = __ldg(in + e);
+        if (transpose) vb = __ldg(iHs + e);
       }
-      pf[l] = v;
+      pf.a[l] = va;
+      pf.b[l] = vb;
     }
   };
-  auto stage = [&](int b, const double (&pf)[NL]) {
+  auto stage = [&](int b, const Pf& pf) {
 #pragma unroll
     for (int l = 0; l < NL; ++l)
-      if (t + l * FT_T < PX * PY) pl[b][t + l * FT_T] = pf[l];
+      if (t + l * FT_T < PX * PY) pl[b][t + l * FT_T] = transpose ? pf.a[l] * pf.b[l] : pf.a[l];
   };
   const int zb = max(0, z0 - R), ze = min(g.nz, z1 + R);  // input planes that exist
   const int x = x0 + tx;
-  // output plane z is complete once input plane z + R is in (or the domain ends)
-  auto flush = [&](int z) {
+  // output plane z is complete once input plane z + R is in (or the domain ends); forward
+  // mode scales by 1/Hs of the output (ih, loaded at the start of the step)
+  auto flush = [&](int z, const double (&ih)[ROWS]) {
 #pragma unroll
     for (int h = 0; h < ROWS; ++h) {
       const int y = y0 + ty + h * FT_YT;
       if (x < g.nx && y < g.ny && z >= z0 && z < z1) {
         const long long e = x + (long long)g.nx * y + pe * z;
-        out[e] = transpose ? acc[h][0] : acc[h][0] * iHs[e];
+        out[e] = transpose ? acc[h][0] : acc[h][0] * ih[h];
       }
 #pragma unroll
       for (int j = 0; j + 1 < NA; ++j) acc[h][j] = acc[h][j + 1];
       acc[h][NA - 1] = 0.0;
     }
   };
+  auto load_ih = [&](int z, double (&ih)[ROWS]) {
+#pragma unroll
+    for (int h = 0; h < ROWS; ++h) {
+      const int y = y0 + ty + h * FT_YT;
+      ih[h] = (!transpose && x < g.nx && y < g.ny && z >= z0 && z < z1)
+                  ? __ldg(iHs + x + (long long)g.nx * y + pe * z) : 0.0;
+    }
+  };
   // input plane zi from smem buffer b; the loads of plane zi + 2 go to F while the FMAs run,
   // plane zi + 1 (fetched one step earlier into S) is staged into the other buffer at the end
-  auto step = [&](int zi, int b, double (&F)[NL], const double (&S)[NL]) {
+  auto step = [&](int zi, int b, Pf& F, const Pf& S) {
     if (zi + 2 < ze) fetch(F, zi + 2);
+    double ih[ROWS];
+    load_ih(zi - R, ih);
     const double* P = pl[b];
 #pragma unroll
     for (int dy = -R; dy <= R + (ROWS - 1) * FT_YT; ++dy) {
@@ -975,15 +991,18 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const d
         }
       }
     }
-    flush(zi - R);
+    flush(zi - R, ih);
     if (zi + 1 == ze)  // drain: outputs whose remaining input planes lie outside the domain
-      for (int z = zi - R + 1; z < z1; ++z) flush(z);
+      for (int z = zi - R + 1; z < z1; ++z) {
+        load_ih(z, ih);
+        flush(z, ih);
+      }
     if (zi + 1 < ze) {
       stage(b ^ 1, S);
       __syncthreads();
     }
   };
-  double pa[NL], pb[NL];
+  Pf pa, pb;
   fetch(pa, zb);
   fetch(pb, zb + 1);
   stage(0, pa);
