@@ -961,10 +961,6 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const d
     if (zi + 2 < ze) fetch(F, zi + 2);
     double ih[ROWS];
     load_ih(zi - R, ih);
-    // accumulators of output planes outside this chunk (the 2R halo planes) get no FMAs
-    bool jl[NA];
-#pragma unroll
-    for (int j = 0; j < NA; ++j) jl[j] = zi - R + j >= z0 && zi - R + j < z1;
     const double* P = pl[b];
 #pragma unroll
     for (int dy = -R; dy <= R + (ROWS - 1) * FT_YT; ++dy) {
@@ -987,7 +983,7 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const d
 #pragma unroll
           for (int j = 0; j < NA; ++j) {
             const int dz = R - j, d2 = dx * dx + dyh * dyh + dz * dz;
-            if (d2 <= (MM >= 0 ? MM : DMAX) && jl[j]) {
+            if (d2 <= (MM >= 0 ? MM : DMAX)) {
               if (MM >= 0) acc[h][j] = fma(w[MM >= 0 ? d2 : 0], v, acc[h][j]);
               else if (d2 <= Mr) acc[h][j] = fma(sw[d2], v, acc[h][j]);
             }
@@ -1273,10 +1269,10 @@ cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, 
                                 const double* in, double* out, int transpose, int sms,
                                 cudaStream_t st) {
   const int tiles = ((g.nx + FT_X - 1) / FT_X) * ((g.ny + FT_Y - 1) / FT_Y);
-  // z chunks: aim at >= 6 blocks per SM (the halo planes of a chunk cost shared loads, not
-  // FMAs: accumulators of planes outside the chunk are skipped), chunks of >= 2R + 2 planes
-  int chunks = std::max(1, (6 * sms + tiles - 1) / tiles);
-  chunks = std::min(chunks, std::max(1, g.nz / (2 * R + 2)));
+  // z chunks: aim at >= 3 blocks per SM, but no chunk thinner than 4R + 4 planes (the 2R
+  // halo planes of a chunk cost FMAs)
+  int chunks = std::max(1, (3 * sms + tiles - 1) / tiles);
+  chunks = std::min(chunks, std::max(1, g.nz / (4 * R + 4)));
   const int zchunk = (g.nz + chunks - 1) / chunks;
   chunks = (g.nz + zchunk - 1) / zchunk;
   const dim3 grid(tiles * chunks);
