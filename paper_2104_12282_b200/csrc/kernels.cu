@@ -324,39 +324,6 @@ __device__ __forceinline__ void issue_plane(const OpArgs& a, double* stg, uint64
   tma_load_3d(stg + L::ee, &a.tm_E, o.xe, j0 - 1, kq - 1, bar);  // element plane kq-1
 }
 
-// The same loads spread over the block's warps (lane 0 of warp w issues load w; warp 0 also
-// arrives with the stage's byte count), so that no single warp carries all the issue work
-// into the next block barrier. The transaction count may run ahead of the arrival: the phase
-// completes only after the arrival AND all bytes.
-template <int MODE>
-__device__ __forceinline__ void issue_plane_spread(const OpArgs& a, double* stg, uint64_t* bar,
-                                                   const TileOrigin& o, int i0, int j0, int kq,
-                                                   int w) {
-  using L = Lay<MODE>;
-  constexpr int NLOAD = MODE == OP_PCG ? 7 : 3;
-  static_assert(NLOAD <= BY, "one load per warp");
-  if (w == 0) mbar_expect_tx(bar, L::bytes);
-  if (MODE == OP_PCG) {
-    switch (w) {
-      case 0: tma_load_3d(stg + R_OFF, &a.tm_in, o.xv, 3 * (j0 - 1), kq, bar); break;
-      case 1: tma_load_3d(stg + QO_OFF, &a.tm_qold, o.xv, 3 * (j0 - 1), kq, bar); break;
-      case 2: tma_load_3d(stg + PO_OFF, &a.tm_pold, o.xv, 3 * (j0 - 1), kq, bar); break;
-      case 3: tma_load_3d(stg + UO_OFF, &a.tm_uown, o.xv, 3 * j0, kq, bar); break;
-      case 4: tma_load_3d(stg + DI_OFF, &a.tm_dinv, o.xv, j0 - 1, kq, bar); break;
-      case 5: tma_load_3d(stg + L::mk, &a.tm_mask, o.xm, j0 - 1, kq, bar); break;
-      case 6: tma_load_3d(stg + L::ee, &a.tm_E, o.xe, j0 - 1, kq - 1, bar); break;
-      default: break;
-    }
-  } else {
-    switch (w) {
-      case 0: tma_load_3d(stg + R_OFF, &a.tm_in, o.xv, 3 * (j0 - 1), kq, bar); break;
-      case 1: tma_load_3d(stg + L::mk, &a.tm_mask, o.xm, j0 - 1, kq, bar); break;
-      case 2: tma_load_3d(stg + L::ee, &a.tm_E, o.xe, j0 - 1, kq - 1, bar); break;
-      default: break;
-    }
-  }
-}
-
 // per-thread state carried from one node plane to the next
 struct Carry {
   double F[12];        // Walsh face of the node plane (the next element's lower face)
@@ -572,11 +539,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
     }
     __syncthreads();  // CD of this plane complete; stage s consumed by every warp
     // (issuing from warp BY-1, which has no owned row, measured the same: 71.8 vs 71.4 us)
-#if TOMO_TMA_SPREAD
-    if (tx == 0 && it + NS < nit) issue_plane_spread<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS, ty);
-#else
     if (t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
-#endif
     // (a segment's last NS steps issue nothing, so the next segment starts with free stages)
 
     if (it >= 2 && mine) {

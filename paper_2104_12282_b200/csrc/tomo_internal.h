@@ -113,9 +113,6 @@ constexpr int OP_GSREG_APPLY = TOMO_GSREG_APPLY, OP_GSREG_PCG = TOMO_GSREG_PCG;
 #define TOMO_PINGPONG_PCG 0
 #endif
 constexpr bool OP_PINGPONG_PCG = TOMO_PINGPONG_PCG != 0;
-#ifndef TOMO_TMA_SPREAD
-#define TOMO_TMA_SPREAD 1  // refill TMA loads issued by lane 0 of several warps (kernels.cu)
-#endif
 #ifndef TOMO_OP_NS_APPLY
 #define TOMO_OP_NS_APPLY 6
 #endif
