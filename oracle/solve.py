@@ -73,3 +73,51 @@ def pcg(apply_A, dinv, f, x0=None, tol=1e-10, max_iters=100000, callback=None,
         rz = rz_new
         p = z + beta * p
     return u, k, False, rnorm / fnorm
+
+
+def pcg_single_pass(apply_A, dinv, f, x0=None, tol=1e-10, max_iters=100000, callback=None):
+    """The single-reduction reformulation of the same Jacobi-PCG (reading R1; the
+    recurrence the fused CUDA kernel runs, restated here from that description - no code is
+    shared). Mathematically it produces the iterates of pcg() above: with q = A p,
+    r_{k+1}.z_{k+1} = r.z - 2 alpha z.q + alpha^2 q.D^-1.q, so beta needs no second
+    reduction. "Launch" k forms
+        r_k = r_{k-1} - alpha_{k-1} q_{k-1},  z_k = D^-1 r_k,  p_k = z_k + beta_{k-1} p_{k-1},
+        u_k = u_{k-1} + alpha_{k-1} p_{k-1},  q_k = A p_k,
+    reduces p.q, r.z, r.r, z.q, q.D^-1.q, stops when ||r_k|| <= tol ||f|| (count k = the
+    products that contributed to u), else alpha_k = r.z / p.q and
+    beta_k = (r.z - 2 alpha_k z.q + alpha_k^2 q.D^-1.q) / r.z.
+    In floating point the predicted numerator differs from the explicit one by rounding that
+    is amplified where the residual drops sharply; at high contrast the two recurrences then
+    follow different (equally valid) finite-precision trajectories. Pinned against pcg() on
+    well-conditioned systems (tests/test_oracle_fem.py). Returns as pcg()."""
+    f = np.asarray(f, dtype=np.float64)
+    fnorm = np.linalg.norm(f)
+    if fnorm == 0.0:
+        return np.zeros_like(f), 0, True, 0.0
+    u = np.zeros_like(f) if x0 is None else np.array(x0, dtype=np.float64)
+    r_prev = f - apply_A(u) if np.any(u) else f.copy()
+    q_prev = np.zeros_like(f)
+    p_prev = np.zeros_like(f)
+    alpha = beta = 0.0
+    k = 0
+    while True:
+        r = r_prev - alpha * q_prev
+        z = dinv * r
+        p = z + beta * p_prev
+        u = u + alpha * p_prev
+        q = apply_A(p)
+        pq, rz, rr, zq, qdq = p @ q, r @ z, r @ r, z @ q, q @ (dinv * q)
+        rel = np.sqrt(rr) / fnorm
+        if callback is not None:
+            callback(k, rel)
+        if np.sqrt(rr) <= tol * fnorm:
+            return u, k, True, rel
+        if k >= max_iters:
+            return u, k, False, rel
+        if not pq > 0.0:
+            raise Breakdown(f"p^T A p = {pq} <= 0 at launch {k} (SPEC:173)")
+        alpha_k = rz / pq
+        beta = (rz - 2.0 * alpha_k * zq + alpha_k * alpha_k * qdq) / rz
+        alpha = alpha_k
+        r_prev, q_prev, p_prev = r, q, p
+        k += 1

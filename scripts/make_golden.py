@@ -128,12 +128,43 @@ def cfg4(idx_variant, n_sample=4096, seed=44):
             json.dump(meta, f)
 
 
+def single_pass(names):
+    """Record the single-pass reformulation's iteration count to 1e-10 (oracle.solve.
+    pcg_single_pass, reading R1) next to the textbook count in existing goldens: the
+    iteration-count pin of the CUDA path, whose kernel runs that recurrence."""
+    from oracle import fem, solve
+    for name in names:
+        if name.startswith("cfg4"):
+            idx, variant = "abcde".index(name[4]), name.split("_", 1)[1]
+            p = inputs.cfg4(idx)
+            rho = inputs.density_void07(p) if variant == "void07" else inputs.density_uniform(p, 0.5)
+        else:
+            p, rho = inputs.CONFIGS[name], inputs.density_for(name)
+        op = OracleProblem(p)
+        E = op.E(rho)
+        A = fem.apply_bc(fem.assemble(op.edof, E, op.KE, op.n_dof), op.fixed)
+        dinv = 1.0 / fem.jacobi_diag(E, op.KE, op.edof, op.fixed)
+        t = time.time()
+        _, k, conv, rel = solve.pcg_single_pass(A.__matmul__, dinv, op.f, tol=1e-10, max_iters=200000)
+        for suffix in ("_solve.json", "_sampled.json"):
+            path = os.path.join(GOLD, name + suffix)
+            if os.path.exists(path):
+                with open(path) as fh:
+                    meta = json.load(fh)
+                meta["pcg_single_pass_iters_1e-10"] = int(k)
+                with open(path, "w") as fh:
+                    json.dump(meta, fh, indent=None if suffix == "_sampled.json" else 1)
+        print(name, "single-pass", k, conv, rel, time.time() - t, flush=True)
+
+
 if __name__ == "__main__":
     for a in sys.argv[1:]:
         if a == "cfg1":
             cfg1()
         elif a == "cfg3":
             cfg3_sampled()
+        elif a.startswith("sp:"):     # sp:cfg4a_void07 - single-pass count into that golden
+            single_pass([a[3:]])
         elif a.startswith("cfg4:"):   # cfg4:0void07, cfg4:1uniform, ...
             cfg4(a.split(":", 1)[1])
         else:

@@ -74,28 +74,29 @@ def _gold(name):
 
 def test_cfg2_mbb_half_beam_against_tight_oracle():
     """configs[2] against the oracle's tight (1e-12) solution (reading A14). The GPU solves
-    to 1e-10 as BJ states: compliance is quadratic in the energy error (App. A-6) and must
-    agree to 1e-9; u and dc to max(1e-8, 4 delta) with delta the solver-noise floor measured
-    as the GPU's own 1e-10 vs 1e-12 difference; at 1e-12 both sides agree to 1e-8."""
+    to 1e-10 as BJ states: c must agree to 1e-9 (quadratic in the energy error, App. A-6);
+    u, dc and P^T dc to max(1e-8, 2 delta_floor) with delta_floor the ORACLE's own 1e-10 vs
+    1e-12 difference (stored in the golden); at 1e-12 the GPU agrees to 1e-8 as well."""
     meta, gold = _gold("cfg2")
+    df = meta["delta_floor"]
     p = inputs.CFG2
     rho = inputs.density_for("cfg2")
     t = ctx(p)
     u_g, c, dcf, info = t.evaluate(gpu(rho), tol=1e-10)
     assert info.converged >= 1
-    assert abs(info.iterations - meta["pcg_iters_1e-10"]) <= max(3, 0.02 * meta["pcg_iters_1e-10"])
+    # iteration count: the single-pass recurrence (reading R1) vs its CPU run, textbook beside
+    k_sp = meta.get("pcg_single_pass_iters_1e-10")
+    k_ref = k_sp if k_sp is not None else meta["pcg_iters_1e-10"]
+    assert abs(info.iterations - k_ref) <= max(3, 0.02 * k_ref), (info.iterations, k_sp, meta["pcg_iters_1e-10"])
     assert abs(c - meta["c"]) <= 1e-9 * abs(meta["c"])
+    assert rel(cpu(u_g), gold["u"]) <= max(1e-8, 2 * df["u"])
+    dc = cpu(t.sensitivity(gpu(rho), u_g))
+    assert rel(dc, gold["dc"]) <= max(1e-8, 2 * df["dc"])
+    assert rel(cpu(dcf), gold["dcf"]) <= max(1e-8, 2 * df["dcf"])
     u12, info12 = t.solve(gpu(rho), tol=1e-12, max_iters=200000)
     assert info12.converged >= 1
     assert rel(cpu(u12), gold["u"]) <= 1e-8
-    dc12 = cpu(t.sensitivity(gpu(rho), u12))
-    assert rel(dc12, gold["dc"]) <= 1e-8
-    delta = rel(cpu(u_g), cpu(u12))
-    assert rel(cpu(u_g), gold["u"]) <= max(1e-8, 4 * delta), delta
-    dc = cpu(t.sensitivity(gpu(rho), u_g))
-    bar_dc = max(1e-8, 4 * rel(dc, dc12))
-    assert rel(dc, gold["dc"]) <= bar_dc
-    assert rel(cpu(dcf), gold["dcf"]) <= bar_dc
+    assert rel(cpu(t.sensitivity(gpu(rho), u12)), gold["dc"]) <= 1e-8
     # operator-level parity on the oracle's own u (no solver noise)
     dc_on_gold = cpu(t.sensitivity(gpu(rho), gpu(gold["u"])))
     assert rel(dc_on_gold, gold["dc"]) <= 1e-12
@@ -222,10 +223,11 @@ def test_cfg3_loop_20_iterations():
 
 def test_cfg3_against_sampled_tight_oracle_if_present():
     """configs[3], the metric's workload, against the oracle's own tight (1e-12) solve
-    (tests/golden/cfg3_sampled.json, written by scripts/make_golden.py cfg3 - about an hour of
-    host time, so sampled: c, norms and seeded entries of u, dc, P^T dc). Bars as for cfg2
-    (reading A14): c to 1e-9; u, dc, dcf to max(1e-8, 4 delta) with delta the GPU's own 1e-10
-    vs 1e-12 difference on the same samples."""
+    (tests/golden/cfg3_sampled.json, written by scripts/make_golden.py cfg3 - about 1.5 h of
+    host time, so sampled: c, the full-vector norms and seeded entries of u, dc, P^T dc).
+    Bars (reading A14): c to 1e-9; u, dc, dcf to max(1e-8, 2 delta_floor) with delta_floor
+    the ORACLE's own 1e-10 vs 1e-12 difference where the golden records it (else the GPU's
+    own, with a 4x margin); the GPU at 1e-12 to 1e-8."""
     path = os.path.join(GOLD, "cfg3_sampled.json")
     if not os.path.exists(path):
         pytest.skip("cfg3 sampled golden not generated (python scripts/make_golden.py cfg3)")
@@ -245,8 +247,15 @@ def test_cfg3_against_sampled_tight_oracle_if_present():
     gu, gdc, gdcf = np.array(g["u"]), np.array(g["dc"]), np.array(g["dcf"])
     assert abs(c12 - g["c"]) <= 1e-9 * abs(g["c"])
     assert abs(c10 - g["c"]) <= 1e-9 * abs(g["c"])
-    for a12, a10, gold in ((su(u12), su(u10), gu), (se(dc12), se(dc10), gdc),
-                           (se(dcf12), se(dcf10), gdcf)):
-        delta = rel(a10, a12)
-        assert rel(a12, gold) <= 1e-8
-        assert rel(a10, gold) <= max(1e-8, 4 * delta), delta
+    df = g.get("delta_floor")
+    for key, a12, a10, gold, full10, norm in (
+            ("u", su(u12), su(u10), gu, cpu(u10), g["norm_u"]),
+            ("dc", se(dc12), se(dc10), gdc, dc10, g["norm_dc"]),
+            ("dcf", se(dcf12), se(dcf10), gdcf, cpu(dcf10), g["norm_dcf"])):
+        bar = max(1e-8, 2 * df[key]) if df else max(1e-8, 4 * rel(a10, a12))
+        assert rel(a12, gold) <= 1e-8, key
+        assert rel(a10, gold) <= bar, (key, rel(a10, gold), bar)
+        # the full-vector norm of the oracle's solution
+        assert abs(np.linalg.norm(full10) - norm) <= bar * norm, key
+    if g.get("pcg_iters_1e-10"):
+        print(f"cfg3: GPU {info10.iterations} iterations, oracle textbook {g['pcg_iters_1e-10']}")

@@ -366,6 +366,45 @@ def test_pcg_toy_systems():
         solve.pcg(lambda v: -v, np.ones(2), np.array([1.0, 1.0]))
 
 
+def test_pcg_single_pass_toy_systems_and_finite_termination():
+    """oracle.solve.pcg_single_pass (reading R1) against closed forms and CG theory: the
+    identity needs 1 iteration; the 2x2 system of SPEC:176 gives (1/11, 7/11); on an SPD
+    matrix with n distinct eigenvalues Krylov optimality terminates in n iterations, like
+    textbook pcg; the breakdown rule holds."""
+    f = np.array([1.0, -2.0, 3.0])
+    u, k, conv, _ = solve.pcg_single_pass(lambda v: v, np.ones(3), f, tol=1e-12)
+    assert k == 1 and conv and np.array_equal(u, f)
+    A = np.array([[4.0, 1.0], [1.0, 3.0]])
+    u, k, conv, _ = solve.pcg_single_pass(lambda v: A @ v, 1.0 / np.diag(A), np.array([1.0, 2.0]),
+                                          tol=1e-14)
+    assert conv and np.allclose(u, [1 / 11, 7 / 11], rtol=1e-14)
+    rng = np.random.default_rng(4)
+    Q, _ = np.linalg.qr(rng.standard_normal((8, 8)))
+    B = Q @ np.diag(np.linspace(1.0, 4.0, 8)) @ Q.T
+    b = rng.standard_normal(8)
+    x = np.linalg.solve(B, b)
+    for fn in (solve.pcg, solve.pcg_single_pass):
+        u, k, conv, _ = fn(lambda v: B @ v, np.ones(8), b, tol=1e-10)
+        assert conv and k <= 8 and np.allclose(u, x, rtol=1e-9)
+    with pytest.raises(solve.Breakdown):
+        solve.pcg_single_pass(lambda v: -v, np.ones(2), np.array([1.0, 1.0]))
+
+
+def test_pcg_single_pass_matches_textbook_fem():
+    """On a moderately conditioned FE system the single-pass recurrence reproduces textbook
+    Jacobi-PCG: the same iteration count (+-1) and the same solution to the tolerance."""
+    p, rho = inputs.random_problem(8, 4, 4, seed=12, lo=0.2)
+    op = OracleProblem(p)
+    E = op.E(rho)
+    K = op.Khat(rho)
+    dinv = op.dinv(rho)
+    u1, k1, c1, _ = solve.pcg(K.__matmul__, dinv, op.f, tol=1e-10)
+    u2, k2, c2, _ = solve.pcg_single_pass(K.__matmul__, dinv, op.f, tol=1e-10)
+    assert c1 and c2 and abs(k1 - k2) <= 1
+    assert np.linalg.norm(u1 - u2) <= 1e-8 * np.linalg.norm(u1)
+    assert E.size == p.n_elem
+
+
 def test_pcg_matches_direct_fem():
     p, rho = inputs.random_problem(6, 3, 3, seed=11, lo=0.2)
     op = OracleProblem(p)
