@@ -5,6 +5,7 @@
 #        | time:<python script args>        (outputs under gpurun_out/TAG_*)
 TAG=$1; shift
 O=gpurun_out; mkdir -p $O
+DPM=sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/${TAG}_gpu.txt 2>&1
 for S in "$@"; do
   case "$S" in
@@ -19,8 +20,12 @@ for S in "$@"; do
       ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches.csv \
         python scripts/prof_step.py cfg3 12 > $O/${TAG}_ncu_ll.log 2>&1; tail -2 $O/${TAG}_ncu_ll.log ;;
     ncu:*) K=${S#ncu:}; TOMO_NO_GRAPH=1 python scripts/prof_step.py cfg3 12 > $O/${TAG}_plain.log 2>&1 && \
-      TOMO_NO_GRAPH=1 ncu --set full --clock-control none --import-source on -k regex:"$K" -s 4 -c 2 \
+      TOMO_NO_GRAPH=1 ncu --set full --metrics $DPM --clock-control none --import-source on -k regex:"$K" -s 4 -c 2 \
         -o $O/${TAG}_prof python scripts/prof_step.py cfg3 12 > $O/${TAG}_ncu.log 2>&1; tail -2 $O/${TAG}_ncu.log ;;
+    ncuall) TOMO_NO_GRAPH=1 python scripts/prof_step.py cfg3 6 > $O/${TAG}_plain.log 2>&1 && \
+      TOMO_NO_GRAPH=1 ncu --set full --metrics $DPM --clock-control none --import-source on \
+        -k regex:"k_op|k_sens|k_filter_t|k_oc" -c 12 -o $O/${TAG}_all python scripts/prof_step.py cfg3 6 \
+        > $O/${TAG}_ncuall.log 2>&1; tail -2 $O/${TAG}_ncuall.log ;;
     time:*) timeout 900 python ${S#time:} > $O/${TAG}_time.log 2>&1; tail -5 $O/${TAG}_time.log ;;
   esac
 done

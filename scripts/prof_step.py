@@ -1,4 +1,6 @@
-"""Short profiling driver: a few fused PCG iterations (K_A + K_B) at a BASELINE config, for ncu.
+"""Short profiling driver: a few fused PCG iterations, the sensitivity, the filter transpose
+and one OC update at a BASELINE config, for ncu (run with TOMO_NO_GRAPH=1 so that the PCG
+launches are ordinary kernel launches).
    python scripts/prof_step.py [cfg] [iters]"""
 import os
 import sys
@@ -16,5 +18,7 @@ rho = torch.tensor(inputs.density_for(cfg), dtype=torch.float64, device="cuda:0"
 u, info = t.solve(rho, tol=1e-10, max_iters=iters)
 dc = t.sensitivity(rho, u)
 dcf = t.filter(dc, transpose=True)
+dv = t.volume_grad()
+xn, lam, steps = t.oc_update(rho, dcf, dv, 0.3)
 torch.cuda.synchronize()
-print("ok", cfg, info.as_dict())
+print("ok", cfg, info.as_dict(), lam, steps)
