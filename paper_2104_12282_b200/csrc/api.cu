@@ -832,7 +832,7 @@ extern "C" int tomo_sensitivity(tomo_ctx* c, const double* d_rho, const double* 
   if (!check_ptr(d_rho) || !check_ptr(d_u) || !check_ptr(d_dc) || (d_ce && !check_ptr(d_ce)))
     return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
   LAUNCH(c, launch_sens(c->g, c->w, d_rho, d_u, c->dmask(), c->penal, c->E0 - c->Emin, c->Emin,
-                        d_dc, d_ce, c->part(), c->nb_s, c->scal(), energy_out ? 1 : 0, c->st));
+                        d_dc, d_ce, c->part(), (int)c->n_part, c->scal(), energy_out ? 1 : 0, c->st));
   if (energy_out) {
     CK(c, cudaMemcpyAsync(energy_out, &c->scal()->energy, sizeof(double), cudaMemcpyDeviceToHost, c->st));
     CK(c, cudaStreamSynchronize(c->st));
@@ -893,7 +893,7 @@ int evaluate_dev(tomo_ctx* c, const double* d_rho, double* d_u, double* d_dc, do
   double* dc = d_dc ? d_dc : c->t0();
   LAUNCH(c, launch_compliance(d_u, c->ld(), c->lv(), (int)c->load_dofs.size(), c->scal(), c->st));
   LAUNCH(c, launch_sens(c->g, c->w, d_rho, d_u, c->dmask(), c->penal, c->E0 - c->Emin, c->Emin,
-                        dc, nullptr, c->part(), c->nb_s, c->scal(), 0, c->st));
+                        dc, nullptr, c->part(), (int)c->n_part, c->scal(), 0, c->st));
   LAUNCH(c, run_filter(c, dc, d_dcf, 1));
   if (c_out) {
     CK(c, cudaMemcpyAsync(c_out, &c->scal()->comp, sizeof(double), cudaMemcpyDeviceToHost, c->st));

@@ -758,48 +758,70 @@ __global__ void k_compliance(const double* u, const int64_t* dofs, const double*
   if (threadIdx.x == 0) s->comp = tot;
 }
 
+// Sensitivity (Eq. 5) by element columns: a 32 x 8 block, lane tx <-> node column i0+tx of
+// node rows j and j+1 (j = j0 + ty), marching along z through a chunk of node planes. Each
+// node plane is loaded once per thread (6 values, masked), the x-neighbour's corners come
+// by warp shuffle and the lower face is carried from the previous plane, so an element
+// costs 6 loads instead of 24 gathers; lane 31 only supplies corners. ce = w^T D w.
+constexpr int SENS_X = 31, SENS_BY = 8;
 __global__ void __launch_bounds__(256) k_sens(Grid g, Walsh W, const double* __restrict__ rho,
                                               const double* __restrict__ u,
                                               const uint8_t* __restrict__ mask, double penal,
                                               double dE, double Emin, double* __restrict__ dc,
                                               double* __restrict__ ce_out, double* partials,
-                                              Scal* s, int want_energy) {
+                                              Scal* s, int want_energy, int zchunk) {
   __shared__ double red[32];
   __shared__ int s_flag;
-  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tiles_x = (g.nx + SENS_X - 1) / SENS_X, tiles = tiles_x * ((g.ny + SENS_BY - 1) / SENS_BY);
+  const int tile = blockIdx.x % tiles, ch = blockIdx.x / tiles;
+  const int i0 = (tile % tiles_x) * SENS_X, j = (tile / tiles_x) * SENS_BY + ty;
+  const int k0 = ch * zchunk, k1 = min(g.nz, k0 + zchunk);  // elements k0 .. k1-1
+  const int in = i0 + tx;                                    // this lane's node column
+  const bool node_ok = in <= g.nx && j < g.ny;
+  const bool elem_ok = tx < SENS_X && in < g.nx && j < g.ny;
   double energy = 0.0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.ne; e += stride) {
-    const int i = (int)(e % g.nx);
-    const int j = (int)((e / g.nx) % g.ny);
-    const int k = (int)(e / ((long long)g.nx * g.ny));
-    double cv[8][3];
+  double Flo[12], Fhi[12];
+  auto face = [&](int k, double (&F)[12]) {  // Walsh face of node plane k for element (i, j)
+    double a0[3] = {0.0, 0.0, 0.0}, a1[3] = {0.0, 0.0, 0.0};
+    if (node_ok) {
+      const long long n0 = node_dense(g, in, j, k), n1 = node_dense(g, in, j + 1, k);
+      const unsigned m0 = __ldg(mask + mask_index(g, in, j, k));
+      const unsigned m1 = __ldg(mask + mask_index(g, in, j + 1, k));
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      int ax, ay, az;
-      corner_offset(a, ax, ay, az);
-      const long long n = node_dense(g, i + ax, j + ay, k + az);
-      const unsigned m = __ldg(mask + mask_index(g, i + ax, j + ay, k + az));
-#pragma unroll
-      for (int c = 0; c < 3; ++c) cv[a][c] = ((m >> c) & 1u) ? 0.0 : __ldg(u + 3 * n + c);
+      for (int c = 0; c < 3; ++c) {
+        a0[c] = ((m0 >> c) & 1u) ? 0.0 : __ldg(u + 3 * n0 + c);
+        a1[c] = ((m1 >> c) & 1u) ? 0.0 : __ldg(u + 3 * n1 + c);
+      }
     }
-    double Flo[12], Fhi[12];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      face_from(cv[0][c], cv[1][c], cv[3][c], cv[2][c], Flo, c);
-      face_from(cv[4][c], cv[5][c], cv[7][c], cv[6][c], Fhi, c);
+      const double b0 = __shfl_down_sync(0xffffffffu, a0[c], 1);
+      const double b1 = __shfl_down_sync(0xffffffffu, a1[c], 1);
+      face_from(a0[c], b0, a1[c], b1, F, c);
     }
-    const double ce = element_energy(Flo, Fhi, W);
-    const double r = rho[e];
-    dc[e] = -penal * pow(r, penal - 1.0) * dE * ce;  // Eq. 5 with dE = E0 - Emin (A5)
-    if (ce_out) ce_out[e] = ce;
-    if (want_energy) energy = fma(Emin + pow(r, penal) * dE, ce, energy);
+  };
+  face(k0, Flo);
+  for (int k = k0; k < k1; ++k) {
+    face(k + 1, Fhi);
+    if (elem_ok) {
+      const long long e = in + (long long)g.nx * (j + (long long)g.ny * k);
+      const double ce = element_energy(Flo, Fhi, W);
+      const double r = rho[e];
+      dc[e] = -penal * pow(r, penal - 1.0) * dE * ce;  // Eq. 5 with dE = E0 - Emin (A5)
+      if (ce_out) ce_out[e] = ce;
+      if (want_energy) energy = fma(Emin + pow(r, penal) * dE, ce, energy);
+    }
+#pragma unroll
+    for (int q = 0; q < 12; ++q) Flo[q] = Fhi[q];
   }
   if (!want_energy) return;
   const double bs = block_sum(energy, red);
-  if (threadIdx.x == 0) partials[blockIdx.x] = bs;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0 && threadIdx.y == 0) partials[b] = bs;
   if (arrive_last(&s->cntR, gridDim.x, &s_flag)) {
     const double tot = sum_partials(partials, gridDim.x, 1, 0, red);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
       s->energy = tot;
       s->cntR = 0;
       __threadfence();
@@ -1239,10 +1261,16 @@ cudaError_t launch_compliance(const double* u, const int64_t* ldofs, const doubl
 }
 cudaError_t launch_sens(const Grid& g, const Walsh& w, const double* rho, const double* u,
                         const uint8_t* mask, double penal, double dE, double Emin,
-                        double* dc, double* ce, double* partials, int nblocks, Scal* s,
+                        double* dc, double* ce, double* partials, int max_blocks, Scal* s,
                         int want_energy, cudaStream_t st) {
-  k_sens<<<nblocks, 256, 0, st>>>(g, w, rho, u, mask, penal, dE, Emin, dc, ce, partials, s,
-                                  want_energy);
+  const int tiles = ((g.nx + SENS_X - 1) / SENS_X) * ((g.ny + SENS_BY - 1) / SENS_BY);
+  int chunks = std::max(1, std::min(g.nz, (4 * 148 + tiles - 1) / tiles));
+  chunks = std::max(1, std::min(chunks, max_blocks / std::max(1, tiles)));
+  const int zchunk = (g.nz + chunks - 1) / chunks;
+  chunks = (g.nz + zchunk - 1) / zchunk;
+  if (want_energy && tiles * chunks > max_blocks) return cudaErrorInvalidValue;  // partials
+  k_sens<<<tiles * chunks, dim3(32, SENS_BY), 0, st>>>(g, w, rho, u, mask, penal, dE, Emin, dc, ce,
+                                                       partials, s, want_energy, zchunk);
   return cudaGetLastError();
 }
 cudaError_t launch_filter_sums(const Grid& g, const int* taps, const double* w, int ntaps,

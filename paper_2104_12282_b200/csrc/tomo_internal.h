@@ -166,7 +166,7 @@ cudaError_t launch_compliance(const double* u, const int64_t* ldofs, const doubl
                               int nloads, Scal* s, cudaStream_t st);
 cudaError_t launch_sens(const Grid& g, const Walsh& w, const double* rho, const double* u,
                         const uint8_t* mask, double penal, double dE, double Emin,
-                        double* dc, double* ce, double* partials, int nblocks, Scal* s,
+                        double* dc, double* ce, double* partials, int max_blocks, Scal* s,
                         int want_energy, cudaStream_t st);
 cudaError_t launch_filter_sums(const Grid& g, const int* taps, const double* w, int ntaps,
                                double* Hs, double* iHs, int* counts, cudaStream_t st);
