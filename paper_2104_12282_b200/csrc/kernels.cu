@@ -417,6 +417,9 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   const int fdb = ty * DB_W + org.ov + tx, fdo = fdb + DB_W;
   const int fmb = ty * MB_W + org.om + tx, fmo = fmb + MB_W;
   const int fe = ty * E_W + org.oe + tx;                 // element (tx, ty)
+  // every stage index this thread will read lies inside its piece of the stage
+  TCHECK(fvb >= 0 && fvo + 2 * VB_W < VB_W * VB_R && (ty >= OY || fuo + 2 * VB_W < VB_W * UB_R));
+  TCHECK(fdo < DB_W * NR && fmo < MB_W * NR && fe < E_W * ER && org.om + TX <= MB_W);
 
   // state carried from one node plane to the next; K_hat u uses the two copies ping-pong (the
   // loop unrolled by two) so that nothing is copied between registers at the end of a step
@@ -463,6 +466,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
       // per store instruction (row-SoA layout)
       if (mine && kn >= kbeg && kn < kend) {
         const int go = g_own + planed * kn;
+        TCHECK(go >= 0 && go + 2 * g.nnx_pad < g.ndof_pad && gi < g.nnx_pad);
         double rz = 0.0, rr = 0.0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -544,6 +548,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
 
     if (it >= 2 && mine) {
       const int gb = g_own + planed * (kn - 1);  // output node plane kn - 1
+      TCHECK(gb >= 0 && gb + 2 * g.nnx_pad < g.ndof_pad);
       double pq = 0.0, zq = 0.0, qdq = 0.0;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -780,12 +785,14 @@ __global__ void __launch_bounds__(256) k_sens(Grid g, Walsh W, const double* __r
   const int in = i0 + tx;                                    // this lane's node column
   const bool node_ok = in <= g.nx && j < g.ny;
   const bool elem_ok = tx < SENS_X && in < g.nx && j < g.ny;
+  const int ipen = (penal == (double)(int)penal && penal >= 1.0 && penal <= 8.0) ? (int)penal : 0;
   double energy = 0.0;
   double Flo[12], Fhi[12];
   auto face = [&](int k, double (&F)[12]) {  // Walsh face of node plane k for element (i, j)
     double a0[3] = {0.0, 0.0, 0.0}, a1[3] = {0.0, 0.0, 0.0};
     if (node_ok) {
       const long long n0 = node_dense(g, in, j, k), n1 = node_dense(g, in, j + 1, k);
+      TCHECK(n0 >= 0 && n1 < g.nn && k <= g.nz);
       const unsigned m0 = __ldg(mask + mask_index(g, in, j, k));
       const unsigned m1 = __ldg(mask + mask_index(g, in, j + 1, k));
 #pragma unroll
@@ -808,9 +815,18 @@ __global__ void __launch_bounds__(256) k_sens(Grid g, Walsh W, const double* __r
       const long long e = in + (long long)g.nx * (j + (long long)g.ny * k);
       const double ce = element_energy(Flo, Fhi, W);
       const double r = rho[e];
-      dc[e] = -penal * pow(r, penal - 1.0) * dE * ce;  // Eq. 5 with dE = E0 - Emin (A5)
+      // r^(p-1): repeated products for integer p (the configs' p = 3; a DP pow costs ~100
+      // instructions), pow otherwise
+      double rp1;
+      if (ipen > 0) {
+        rp1 = 1.0;
+        for (int q = 1; q < ipen; ++q) rp1 *= r;
+      } else {
+        rp1 = pow(r, penal - 1.0);
+      }
+      dc[e] = -penal * rp1 * dE * ce;  // Eq. 5 with dE = E0 - Emin (A5)
       if (ce_out) ce_out[e] = ce;
-      if (want_energy) energy = fma(Emin + pow(r, penal) * dE, ce, energy);
+      if (want_energy) energy = fma(Emin + rp1 * r * dE, ce, energy);
     }
 #pragma unroll
     for (int q = 0; q < 12; ++q) Flo[q] = Fhi[q];
@@ -997,6 +1013,7 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const d
           any |= rh[h];
         }
         if (!any) continue;
+        TCHECK((ty + R + dy) * PX + tx + R + dx < PX * PY);
         const double v = P[(ty + R + dy) * PX + tx + R + dx];
 #pragma unroll
         for (int h = 0; h < ROWS; ++h) {

@@ -8,6 +8,24 @@
 
 namespace tomo {
 
+// Checked build (-DTOMO_CHECKED=1, scripts/build_variants.py checked:TOMO_CHECKED=1): device
+// asserts on shared-memory and global indices of the operator, filter and sensitivity kernels
+// (the memory-safety net in place of compute-sanitizer, which is closed on this pool). A
+// failed check traps, so the launch returns an error instead of reading out of bounds.
+#ifndef TOMO_CHECKED
+#define TOMO_CHECKED 0
+#endif
+#if TOMO_CHECKED
+#define TCHECK(cond) \
+  do {               \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define TCHECK(cond) \
+  do {               \
+  } while (0)
+#endif
+
 // Structured grid of nx*ny*nz hexahedra; (nx+1)(ny+1)(nz+1) nodes.
 // The ABI vectors are dense AoS (DOF 3n+c, node n = i + nnx(j + nny k)). The solver's
 // internal vectors are PADDED ROW-SoA (dof_pad): a node row (j, k) is three component

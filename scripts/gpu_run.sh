@@ -26,6 +26,9 @@ for S in "$@"; do
       TOMO_NO_GRAPH=1 ncu --set full --metrics $DPM --clock-control none --import-source on \
         -k regex:"k_op|k_sens|k_filter_t|k_oc" -c 12 -o $O/${TAG}_all python scripts/prof_step.py cfg3 6 \
         > $O/${TAG}_ncuall.log 2>&1; tail -2 $O/${TAG}_ncuall.log ;;
+    checked) test -f paper_2104_12282_b200/lib/checked.so || python scripts/build_variants.py checked:TOMO_CHECKED=1 > /dev/null
+      TOMO_LIB_PATH=$PWD/paper_2104_12282_b200/lib/checked.so timeout 1500 python -m pytest tests -m gpu -q -rs \
+        -k "parity or edges or errors or twoscale or streams or schedule or cfg4_full or cfg2" > $O/${TAG}_checked.log 2>&1; tail -3 $O/${TAG}_checked.log ;;
     time:*) timeout 900 python ${S#time:} > $O/${TAG}_time.log 2>&1; tail -5 $O/${TAG}_time.log ;;
   esac
 done
