@@ -416,7 +416,9 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   const int fuo = 3 * ty * VB_W + org.ov + tx;           // node row ty+1 in the owned-u box
   const int fdb = ty * DB_W + org.ov + tx, fdo = fdb + DB_W;
   const int fmb = ty * MB_W + org.om + tx, fmo = fmb + MB_W;
-  const int fe = ty * E_W + org.oe + tx;                 // element (tx, ty)
+  // element (tx, ty); lane 31's element lies outside the tile and its result is never read:
+  // it reads lane 30's modulus instead of one past the box (the checked build found this)
+  const int fe = ty * E_W + org.oe + min(tx, TX - 2);
   // every stage index this thread will read lies inside its piece of the stage
   TCHECK(fvb >= 0 && fvo + 2 * VB_W < VB_W * VB_R && (ty >= OY || fuo + 2 * VB_W < VB_W * UB_R));
   TCHECK(fdo < DB_W * NR && fmo < MB_W * NR && fe < E_W * ER && org.om + TX <= MB_W);
