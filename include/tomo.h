@@ -225,6 +225,10 @@ int tomo_bench_dfma(tomo_ctx* ctx, double* gflops_out, double* ms_out);
  * every PCG solve writes d_hist[k] = r_k^T r_k (k < n; the relative residual is
  * sqrt(d_hist[k]) / ||f||). d_hist: caller-owned device buffer of n doubles; n = 0 stops.  */
 int tomo_set_history(tomo_ctx* ctx, double* d_hist, int n);
+/* PCG beta (default 0): 0 = the single-pass recurrence (reading R1: beta from
+ * the predicted r_{k+1}.z_{k+1}, one pass per iteration); 1 = textbook beta from the explicit
+ * r_{k+1}, one extra reduction pass over r, q, D^-1 per iteration.         */
+int tomo_set_pcg_exact_beta(tomo_ctx* ctx, int on);
 /* PCG loop execution (default 1): 1 = the whole loop as one CUDA graph with a conditional
  * WHILE node (one launch and one read-back per solve); 0 = host-batched launches of the
  * same kernel (what ncu can profile: kernels inside conditional graphs are not captured). */

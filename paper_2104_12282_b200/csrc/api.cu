@@ -59,6 +59,7 @@ struct tomo_ctx {
   OpArgs op_apply_u{}, op_apply_p0{}, op_pcg[2];  // op_pcg[k & 1] for launch k
   cudaGraph_t pcg_graph = nullptr;        // WHILE(not done) { launch even; launch odd }
   bool use_graph = true;                  // tomo_set_graph: graph (1) or host batches (0)
+  bool exact_beta = false;                // tomo_set_pcg_exact_beta: textbook beta (extra pass)
   cudaGraphExec_t pcg_exec = nullptr;
   // multigrid hierarchy (tomo_mg_*): levels 1..L-1 are coarse contexts bound to the caller's
   // MG workspace; the outer flexible-CG vectors of the fine level live there too
@@ -551,7 +552,14 @@ int build_pcg_graph(tomo_ctx* c) {
   a1.cond = h;
   cudaGraphNode_t n0, n1;
   CK(c, add_pcg_node(body, &n0, nullptr, 0, a0, c->op_blocks));
-  CK(c, add_pcg_node(body, &n1, &n0, 1, a1, c->op_blocks));
+  if (c->exact_beta) {
+    cudaGraphNode_t b0, b1;
+    CK(c, add_beta_node(body, &b0, &n0, 1, c->g, c->r(0), c->q(0), c->dinv(), c->scal(), c->part(), c->nb_b));
+    CK(c, add_pcg_node(body, &n1, &b0, 1, a1, c->op_blocks));
+    CK(c, add_beta_node(body, &b1, &n1, 1, c->g, c->r(1), c->q(1), c->dinv(), c->scal(), c->part(), c->nb_b));
+  } else {
+    CK(c, add_pcg_node(body, &n1, &n0, 1, a1, c->op_blocks));
+  }
   CK(c, cudaGraphInstantiate(&c->pcg_exec, c->pcg_graph, 0));
   return TOMO_OK;
 }
@@ -721,6 +729,10 @@ int run_pcg_loop(tomo_ctx* c, int max_iters, Scal* hs_out) {
     for (int i = 0; i < nb; ++i) {
       if (prof && i < 256) CK(c, cudaEventRecord(c->ev[2 * i], c->st));
       LAUNCH(c, launch_op(OP_PCG, c->op_pcg[(k + i) & 1], c->op_blocks, c->st));
+      if (c->exact_beta) {
+        const int par = (k + i) & 1;
+        LAUNCH(c, launch_beta(c->g, c->r(par), c->q(par), c->dinv(), c->scal(), c->part(), c->nb_b, c->st));
+      }
       if (prof && i < 256) CK(c, cudaEventRecord(c->ev[2 * i + 1], c->st));
     }
     const int k_before = hs.k;
@@ -1025,6 +1037,13 @@ extern "C" int tomo_set_history(tomo_ctx* c, double* d_hist, int n) {
   CK(c, cudaMemcpyAsync(&s->hist, &h, sizeof(h), cudaMemcpyHostToDevice, c->st));
   CK(c, cudaMemcpyAsync(&s->hist_n, &n, sizeof(n), cudaMemcpyHostToDevice, c->st));
   CK(c, cudaStreamSynchronize(c->st));
+  return TOMO_OK;
+}
+
+extern "C" int tomo_set_pcg_exact_beta(tomo_ctx* c, int on) {
+  if (!c) return TOMO_EINVAL;
+  c->exact_beta = on != 0;
+  if (c->bound) return build_pcg_graph(c);
   return TOMO_OK;
 }
 

@@ -674,6 +674,45 @@ __global__ void __launch_bounds__(256) k_norm2(Grid g, const double* __restrict_
   }
 }
 
+// Exact-beta variant (tomo_set_pcg_exact_beta; the textbook recurrence of SURVEY §8 a4):
+// after launch k, r_{k+1}^T z_{k+1} from the explicit r_{k+1} = r_k - alpha_k q_k over all
+// nodes, so beta_k = r_{k+1}.z_{k+1} / r_k.z_k replaces the single-pass prediction. One more
+// pass over r, q and D^-1 per iteration (the vectors are not written: the next launch forms
+// r_{k+1} again). Deterministic two-stage reduction; skipped once the solve has stopped.
+__global__ void __launch_bounds__(256) k_beta(Grid g, const double* __restrict__ r,
+                                              const double* __restrict__ q,
+                                              const double* __restrict__ dinv, Scal* s,
+                                              double* partials) {
+  __shared__ double red[32];
+  __shared__ int s_flag;
+  if (*(volatile int*)&s->done) return;
+  const double alpha = *(volatile double*)&s->alpha;
+  double acc = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long plane = (long long)g.nnx_pad * g.nny;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < g.nn_pad; n += stride) {
+    const long long i = n % g.nnx_pad, jk = n / g.nnx_pad;  // padded node, row jk = j + nny k
+    const double d = dinv[n];
+    const long long base = i + 3 * g.nnx_pad * jk;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double rn = fma(-alpha, q[base + c * g.nnx_pad], r[base + c * g.nnx_pad]);
+      acc = fma(d * rn, rn, acc);
+    }
+  }
+  (void)plane;
+  const double b = block_sum(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+  if (arrive_last(&s->cntB, gridDim.x, &s_flag)) {
+    const double tot = sum_partials(partials, gridDim.x, 1, 0, red);
+    if (threadIdx.x == 0) {
+      s->beta = tot / s->rz;
+      s->cntB = 0;
+      __threadfence();
+    }
+  }
+}
+
 __global__ void k_scal_init(Scal* s, double tol_fnorm, int max_iters) {
   s->alpha = 0.0; s->beta = 0.0; s->rz = 0.0; s->rr = 0.0; s->pq = 0.0;
   s->rr_true = 0.0; s->tol_fnorm = tol_fnorm; s->energy = 0.0; s->comp = 0.0;
@@ -1267,6 +1306,24 @@ cudaError_t launch_resid(const Grid& g, const double* q, double* r, const int64_
   k_resid<<<nblk(g.ndof_pad, 256, 148 * 16), 256, 0, st>>>(g.ndof_pad, q, r);
   if (nloads > 0) k_add_loads<<<nblk(nloads, 256, 64), 256, 0, st>>>(r, ldofs, lvals, nloads);
   return cudaGetLastError();
+}
+cudaError_t launch_beta(const Grid& g, const double* r, const double* q, const double* dinv,
+                        Scal* s, double* partials, int nblocks, cudaStream_t st) {
+  k_beta<<<nblocks, 256, 0, st>>>(g, r, q, dinv, s, partials);
+  return cudaGetLastError();
+}
+cudaError_t add_beta_node(cudaGraph_t gr, cudaGraphNode_t* node, const cudaGraphNode_t* deps,
+                          size_t ndeps, const Grid& g, const double* r, const double* q,
+                          const double* dinv, Scal* s, double* partials, int nblocks) {
+  cudaKernelNodeParams kp = {};
+  Grid gg = g;
+  void* args[] = {&gg, (void*)&r, (void*)&q, (void*)&dinv, &s, &partials};
+  kp.func = reinterpret_cast<void*>(k_beta);
+  kp.gridDim = dim3(nblocks);
+  kp.blockDim = dim3(256);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  return cudaGraphAddKernelNode(node, gr, deps, ndeps, &kp);
 }
 cudaError_t launch_norm2(const Grid& g, const double* r, Scal* s, double* partials,
                          int nblocks, cudaStream_t st) {

@@ -178,6 +178,12 @@ cudaError_t launch_scal_init(Scal* s, double tol_fnorm, int max_iters, cudaStrea
 // r = -q + f (sparse f at padded DOF indices)
 cudaError_t launch_resid(const Grid& g, const double* q, double* r, const int64_t* ldofs_pad,
                          const double* lvals, int nloads, cudaStream_t st);
+// exact-beta variant: beta_k from the explicit r_{k+1} (after each PCG launch)
+cudaError_t launch_beta(const Grid& g, const double* r, const double* q, const double* dinv,
+                        Scal* s, double* partials, int nblocks, cudaStream_t st);
+cudaError_t add_beta_node(cudaGraph_t gr, cudaGraphNode_t* node, const cudaGraphNode_t* deps,
+                          size_t ndeps, const Grid& g, const double* r, const double* q,
+                          const double* dinv, Scal* s, double* partials, int nblocks);
 cudaError_t launch_norm2(const Grid& g, const double* r, Scal* s, double* partials,
                          int nblocks, cudaStream_t st);
 cudaError_t launch_compliance(const double* u, const int64_t* ldofs, const double* lvals,

@@ -93,6 +93,7 @@ _SIGS = [
     ("tomo_bench_dfma", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("tomo_set_profiling", C.c_int, [C.c_void_p, C.c_int]),
     ("tomo_set_graph", C.c_int, [C.c_void_p, C.c_int]),
+    ("tomo_set_pcg_exact_beta", C.c_int, [C.c_void_p, C.c_int]),
     ("tomo_set_history", C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     ("tomo_profile_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("tomo_bench_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_double)]),
@@ -424,6 +425,11 @@ class Tomo:
         ms = C.c_double()
         self._check(self.lib.tomo_bench_dfma(self.h, C.byref(gf), C.byref(ms)))
         return gf.value, ms.value
+
+    def set_pcg_exact_beta(self, on: bool):
+        """Textbook beta from the explicit r_{k+1} (one extra pass per iteration) instead of
+        the single-pass prediction (reading R1)."""
+        self._check(self.lib.tomo_set_pcg_exact_beta(self.h, 1 if on else 0))
 
     def set_graph(self, on: bool):
         """PCG loop as one CUDA graph (default) or host-batched launches (ncu-visible)."""

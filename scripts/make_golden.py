@@ -128,6 +128,52 @@ def cfg4(idx_variant, n_sample=4096, seed=44):
             json.dump(meta, f)
 
 
+def ladder(idx_variant, tols=(1e-6, 1e-7, 1e-8, 1e-9, 1e-10, 1e-11, 1e-12), cap=120000,
+           n_sample=4096, seed=44):
+    """configs[4] grids where Jacobi-PCG may not reach 1e-12 (64^3 void 0.7): the oracle's
+    textbook PCG from x0 = 0 to 1e-12 or `cap` iterations, keeping its iterate at the first
+    crossing of every tolerance in `tols` (c, full-vector norms, seeded samples of u and dc,
+    the iteration count) in <name>_ladder.json, so that parity can be checked at the
+    tightest tolerance both solvers reach."""
+    from oracle import fem, solve
+    idx, variant = int(idx_variant[0]), idx_variant[1:]
+    p = inputs.cfg4(idx)
+    rho = inputs.density_void07(p) if variant == "void07" else inputs.density_uniform(p, 0.5)
+    name = f"cfg4{'abcde'[idx]}_{variant}"
+    op = OracleProblem(p)
+    E = op.E(rho)
+    A = fem.apply_bc(fem.assemble(op.edof, E, op.KE, op.n_dof), op.fixed)
+    dinv = 1.0 / fem.jacobi_diag(E, op.KE, op.edof, op.fixed)
+    rng = np.random.default_rng(seed)
+    idof = np.sort(rng.choice(op.n_dof, n_sample, replace=False))
+    iel = np.sort(rng.choice(op.n_e, n_sample, replace=False))
+    snaps = {}
+    pending = sorted(tols, reverse=True)
+    t0 = time.time()
+
+    def record(k, rel, u):
+        c, dc, _, _ = op.evaluate(rho, u)
+        return {"iterations": int(k), "rel_res_recursive": float(rel),
+                "rel_res_true": float(np.linalg.norm(op.f - A @ u) / np.linalg.norm(op.f)),
+                "c": float(c), "norm_u": float(np.linalg.norm(u)), "norm_dc": float(np.linalg.norm(dc)),
+                "u": u[idof].tolist(), "dc": dc[iel].tolist(), "seconds": time.time() - t0}
+
+    def cb(k, rel, u):
+        while pending and rel <= pending[0]:
+            snaps[f"{pending.pop(0):.0e}"] = record(k, rel, u)
+            print(name, "crossed", list(snaps)[-1], "at", k, flush=True)
+
+    u, k, conv, rel = solve.pcg(A.__matmul__, dinv, op.f, tol=min(tols), max_iters=cap, callback_u=cb)
+    meta = {"citation": f"oracle textbook Jacobi-PCG (x0 = 0) on BASELINE.json {p.name} {variant}: its iterate "
+                        "at the first crossing of each recursive tolerance (c = f^T u, Eq. 4; dc Eq. 5; seeded "
+                        "samples). Written by scripts/make_golden.py ladder.",
+            "cap": cap, "final": record(k, rel, u) | {"converged": bool(conv)},
+            "dof_idx": idof.tolist(), "elem_idx": iel.tolist(), "snapshots": snaps}
+    with open(os.path.join(GOLD, f"{name}_ladder.json"), "w") as f:
+        json.dump(meta, f)
+    print(name, "ladder done", k, conv, rel, time.time() - t0, flush=True)
+
+
 def single_pass(names):
     """Record the single-pass reformulation's iteration count to 1e-10 (oracle.solve.
     pcg_single_pass, reading R1) next to the textbook count in existing goldens: the
@@ -165,6 +211,8 @@ if __name__ == "__main__":
             cfg3_sampled()
         elif a.startswith("sp:"):     # sp:cfg4a_void07 - single-pass count into that golden
             single_pass([a[3:]])
+        elif a.startswith("ladder:"):  # ladder:1void07 - tolerance ladder (64^3 void 0.7)
+            ladder(a.split(":", 1)[1])
         elif a.startswith("cfg4:"):   # cfg4:0void07, cfg4:1uniform, ...
             cfg4(a.split(":", 1)[1])
         else:

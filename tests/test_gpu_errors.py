@@ -111,3 +111,27 @@ def test_graph_and_host_batched_loops_bit_identical():
     u3, c3, dcf3, i3 = t.evaluate(rho)
     assert i1.iterations == i2.iterations == i3.iterations and c1 == c2 == c3
     assert torch.equal(u1, u2) and torch.equal(u1, u3) and torch.equal(dcf1, dcf2)
+
+
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg2"])
+def test_exact_beta_variant_matches_textbook_count(cfg):
+    """tomo_set_pcg_exact_beta(1): beta from the explicit r_{k+1} - the textbook recurrence of
+    oracle.solve.pcg. Its iteration count matches the oracle's textbook count
+    (recorded in the golden) to 2%, and its solution the single-pass one to the tolerance."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", f"{cfg}_solve.json")) as f:
+        meta = json.load(f)
+    p = inputs.CONFIGS[cfg]
+    rho = gpu(inputs.density_for(cfg))
+    t = tomo.Tomo(tomo.params_from_problem(p), device=DEV)
+    u1, i1 = t.solve(rho, tol=1e-10)
+    t.set_pcg_exact_beta(True)
+    u2, i2 = t.solve(rho, tol=1e-10)
+    t.set_graph(False)
+    u3, i3 = t.solve(rho, tol=1e-10)
+    assert i2.converged >= 1 and i2.iterations == i3.iterations and torch.equal(u2, u3)
+    k_ref = meta["pcg_iters_1e-10"]
+    assert abs(i2.iterations - k_ref) <= max(3, 0.02 * k_ref), (i2.iterations, k_ref)
+    d = float(torch.linalg.norm(u1 - u2) / torch.linalg.norm(u1))
+    assert d <= 1e-8, d
