@@ -135,3 +135,23 @@ def test_exact_beta_variant_matches_textbook_count(cfg):
     assert abs(i2.iterations - k_ref) <= max(3, 0.02 * k_ref), (i2.iterations, k_ref)
     d = float(torch.linalg.norm(u1 - u2) / torch.linalg.norm(u1))
     assert d <= 1e-8, d
+
+
+def test_residual_history_trace():
+    """tomo_set_history: launch k records r_k^T r_k; its last entry is the reported recursive
+    residual, its first ||f||^2 (x0 = 0), and the trace is the same in graph and host-batched
+    execution."""
+    p, rho = inputs.random_problem(10, 6, 5, seed=8)
+    t = tomo.Tomo(tomo.params_from_problem(p), device=DEV)
+    h = t.set_history(2000)
+    u, info = t.solve(gpu(rho), tol=1e-10)
+    hh = h.cpu().numpy()[: info.iterations + 1]
+    fn = float(np.sqrt((p.ny + 1) * (1.0 / (p.ny + 1)) ** 2))  # cantilever: -1 in ny+1 parts
+    assert abs(np.sqrt(hh[0]) - fn) <= 1e-14 * fn
+    assert abs(np.sqrt(hh[-1]) / fn - info.rel_res_recursive) <= 1e-14
+    assert np.sqrt(hh[-1]) / fn <= 1e-10 and np.all(np.sqrt(hh[:-1]) / fn > 1e-10)
+    t.set_graph(False)
+    h2 = t.set_history(2000)
+    t.solve(gpu(rho), tol=1e-10)
+    assert np.array_equal(h2.cpu().numpy()[: info.iterations + 1], hh)
+    t.set_history(0)
