@@ -1369,7 +1369,7 @@ extern "C" int tomo_solve_mg(tomo_ctx* c, const double* d_rho, int64_t n_e, doub
   CK(c, cudaStreamSynchronize(c->st));
   if (info) {
     info->iterations = k;
-    info->converged = conv;
+    info->converged = !conv ? 0 : (std::sqrt(rrt) <= stop ? 1 : 2);  // as tomo_solve (tomo.h)
     info->rel_res_recursive = std::sqrt(rr) / c->fnorm;
     info->rel_res_true = std::sqrt(rrt) / c->fnorm;
   }
