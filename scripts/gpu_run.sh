@@ -16,9 +16,13 @@ for S in "$@"; do
     bench) timeout 900 python bench.py > $O/${TAG}_bench.log 2>&1; tail -1 $O/${TAG}_bench.log | cut -c1-400 ;;
     benchq) timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_bench.log 2>&1; tail -1 $O/${TAG}_bench.log | cut -c1-400 ;;
     sweep) timeout 1200 python scripts/sweep_cfg4.py > $O/${TAG}_sweep.log 2>&1; tail -3 $O/${TAG}_sweep.log ;;
-    launches) TOMO_NO_GRAPH=1 python scripts/prof_step.py cfg3 12 > $O/${TAG}_plain.log 2>&1 && \
-      ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches.csv \
-        python scripts/prof_step.py cfg3 12 > $O/${TAG}_ncu_ll.log 2>&1; tail -2 $O/${TAG}_ncu_ll.log ;;
+    launches) B="bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+      TOMO_NO_GRAPH=1 python $B > $O/${TAG}_plain.log 2>&1 && \
+      TOMO_NO_GRAPH=1 ncu --metrics gpu__time_duration.sum --clock-control none -s 32000 -c 12000 --csv \
+        --log-file $O/${TAG}_launches.csv python $B > $O/${TAG}_ncu_ll.log 2>&1; tail -2 $O/${TAG}_ncu_ll.log
+      python scripts/launch_list_summary.py $O/${TAG}_launches.csv $O/${TAG}_launch_summary.json \
+        "TOMO_NO_GRAPH=1 ncu --metrics gpu__time_duration.sum -s 32000 -c 12000 $B" > /dev/null ;;
+    report) timeout 1800 python tests/report_configs.py $O/${TAG}_configs_report.json > $O/${TAG}_report.log 2>&1; tail -2 $O/${TAG}_report.log ;;
     ncu:*) K=${S#ncu:}; TOMO_NO_GRAPH=1 python scripts/prof_step.py cfg3 12 > $O/${TAG}_plain.log 2>&1 && \
       TOMO_NO_GRAPH=1 ncu --set full --metrics $DPM --clock-control none --import-source on -k regex:"$K" -s 4 -c 2 \
         -o $O/${TAG}_prof python scripts/prof_step.py cfg3 12 > $O/${TAG}_ncu.log 2>&1; tail -2 $O/${TAG}_ncu.log ;;
