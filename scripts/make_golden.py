@@ -128,7 +128,7 @@ def cfg4(idx_variant, n_sample=4096, seed=44):
             json.dump(meta, f)
 
 
-def ladder(idx_variant, tols=(1e-6, 1e-7, 1e-8, 1e-9, 1e-10, 1e-11, 1e-12), cap=120000,
+def ladder(idx_variant, tols=(1e-4, 1e-5, 1e-6, 1e-7, 1e-8, 1e-9, 1e-10), cap=55000,
            n_sample=4096, seed=44):
     """configs[4] grids where Jacobi-PCG may not reach 1e-12 (64^3 void 0.7): the oracle's
     textbook PCG from x0 = 0 to 1e-12 or `cap` iterations, keeping its iterate at the first
@@ -158,19 +158,23 @@ def ladder(idx_variant, tols=(1e-6, 1e-7, 1e-8, 1e-9, 1e-10, 1e-11, 1e-12), cap=
                 "c": float(c), "norm_u": float(np.linalg.norm(u)), "norm_dc": float(np.linalg.norm(dc)),
                 "u": u[idof].tolist(), "dc": dc[iel].tolist(), "seconds": time.time() - t0}
 
+    def dump(final=None):
+        meta = {"citation": f"oracle textbook Jacobi-PCG (x0 = 0) on BASELINE.json {p.name} {variant}: its "
+                            "iterate at the first crossing of each recursive tolerance and at the iteration cap "
+                            "(c = f^T u, Eq. 4; dc Eq. 5; seeded samples). Written by scripts/make_golden.py ladder.",
+                "cap": cap, "final": final, "dof_idx": idof.tolist(), "elem_idx": iel.tolist(),
+                "snapshots": snaps}
+        with open(os.path.join(GOLD, f"{name}_ladder.json"), "w") as f:
+            json.dump(meta, f)
+
     def cb(k, rel, u):
         while pending and rel <= pending[0]:
             snaps[f"{pending.pop(0):.0e}"] = record(k, rel, u)
             print(name, "crossed", list(snaps)[-1], "at", k, flush=True)
+            dump()
 
     u, k, conv, rel = solve.pcg(A.__matmul__, dinv, op.f, tol=min(tols), max_iters=cap, callback_u=cb)
-    meta = {"citation": f"oracle textbook Jacobi-PCG (x0 = 0) on BASELINE.json {p.name} {variant}: its iterate "
-                        "at the first crossing of each recursive tolerance (c = f^T u, Eq. 4; dc Eq. 5; seeded "
-                        "samples). Written by scripts/make_golden.py ladder.",
-            "cap": cap, "final": record(k, rel, u) | {"converged": bool(conv)},
-            "dof_idx": idof.tolist(), "elem_idx": iel.tolist(), "snapshots": snaps}
-    with open(os.path.join(GOLD, f"{name}_ladder.json"), "w") as f:
-        json.dump(meta, f)
+    dump(record(k, rel, u) | {"converged": bool(conv)})
     print(name, "ladder done", k, conv, rel, time.time() - t0, flush=True)
 
 

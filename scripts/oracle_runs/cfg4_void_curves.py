@@ -50,7 +50,7 @@ if "--direct" in sys.argv:
                      "u_rel_err_pcg": float(np.linalg.norm(u - ud) / np.linalg.norm(ud)),
                      "seconds": time.time() - t0}
     print(json.dumps(out["direct"]), flush=True)
-dst = os.path.join(os.path.dirname(__file__), "..", "..", "tests", "golden",
-                   f"cfg4{sys.argv[1]}_void_oracle_pcg.json")
+dst = os.path.join(os.path.dirname(__file__), "..", "..", "profiles",
+                   f"r2_void_curves_oracle_cfg4{sys.argv[1]}.json")
 with open(dst, "w") as fh:
     json.dump(out, fh, indent=1)
