@@ -23,7 +23,7 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 CASES = [("cfg4a_uniform", 0, "uniform"), ("cfg4a_void07", 0, "void07"),
-         ("cfg4b_uniform", 1, "uniform"), ("cfg4b_void07", 1, "void07")]
+         ("cfg4b_uniform", 1, "uniform")]
 
 
 def gpu(a):
@@ -79,3 +79,43 @@ def test_cfg4_full_solve_parity(name, idx, variant):
         # contrast the count is a property of the finite-precision trajectory and is only
         # reported (reading R1: CPU variants 15,054-15,530, the GPU 11,205)
         assert abs(info.iterations - k_sp) <= max(3, 0.02 * k_sp), (info.iterations, k_sp)
+
+
+def test_cfg4b_void07_at_the_tolerance_both_reach():
+    """64^3 void 0.7: neither the oracle's textbook PCG (relative residual 7.5e-7 after 50,000
+    iterations) nor the GPU (1.6e-8) reaches 1e-10 (reading R1), so parity is
+    checked at the tightest tolerance both reach: t* = the tightest
+    snapshot of the oracle's tolerance ladder (tests/golden/cfg4b_void07_ladder.json: its
+    iterate at the first crossing of each decade and at the 55,000-iteration cap). The GPU
+    solves to t*; c, u and dc (seeded samples, full-vector norms) are compared with the
+    oracle's t* iterate. Both iterates carry an error of the size the oracle's own t* iterate
+    shows against its cap iterate (delta): the bars are 4 delta (c: 4 delta_c, floors 1e-9 /
+    1e-8 as A14)."""
+    path = os.path.join(GOLD, "cfg4b_void07_ladder.json")
+    if not os.path.exists(path):
+        pytest.fail("golden cfg4b_void07_ladder.json missing (python scripts/make_golden.py ladder:1void07)")
+    with open(path) as f:
+        g = json.load(f)
+    assert g["final"] is not None, "ladder run incomplete"
+    tstar = min(g["snapshots"], key=float)
+    snap, fin = g["snapshots"][tstar], g["final"]
+    idof, iel = np.array(g["dof_idx"]), np.array(g["elem_idx"])
+    d_u = rel(np.array(snap["u"]), np.array(fin["u"]))
+    d_dc = rel(np.array(snap["dc"]), np.array(fin["dc"]))
+    d_c = abs(snap["c"] - fin["c"]) / abs(fin["c"])
+    p = inputs.cfg4(1)
+    rho = gpu(inputs.density_void07(p))
+    t = tomo.Tomo(tomo.params_from_problem(p), device=DEV)
+    u, info = t.solve(rho, tol=float(tstar), max_iters=60000)
+    assert info.converged >= 1, info.as_dict()
+    c = t.compliance(u)
+    dc = t.sensitivity(rho, u).cpu().numpy()
+    u = u.cpu().numpy()
+    eu, edc = rel(u[idof], np.array(snap["u"])), rel(dc[iel], np.array(snap["dc"]))
+    ec = abs(c - snap["c"]) / abs(snap["c"])
+    print(f"cfg4b void07 at t* = {tstar}: GPU {info.iterations} it (oracle {snap['iterations']}), "
+          f"c {ec:.1e} (bar {max(1e-9, 4 * d_c):.1e}), u {eu:.1e} (bar {max(1e-8, 4 * d_u):.1e}), "
+          f"dc {edc:.1e} (bar {max(1e-8, 4 * d_dc):.1e})")
+    assert ec <= max(1e-9, 4 * d_c)
+    assert eu <= max(1e-8, 4 * d_u) and edc <= max(1e-8, 4 * d_dc)
+    assert abs(np.linalg.norm(u) - snap["norm_u"]) <= max(1e-8, 4 * d_u) * snap["norm_u"]
