@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   }
 }
 
-// ------------------------------------------------------------------ K_B and reductions
+// ------------------------------------------------------------------ solve-level reductions and vector kernels
 // ||r||^2 over a padded vector (pad entries are 0): the true residual at exit.
 __global__ void __launch_bounds__(256) k_norm2(Grid g, const double* __restrict__ r, Scal* s,
                                                double* partials) {
