@@ -293,7 +293,7 @@ def run_reference(args):
 
 # DRAM bytes per launch of the dominant kernel from one `ncu --set full` capture
 # (dram__bytes_read.sum + dram__bytes_write.sum), see profiles/.
-TRAFFIC = {"cfg3": 272035584}  # r1 session 3 (committed kernel): DRAM read + write per launch (profiles/r1s3_pcg_kernel_ncu.json)
+TRAFFIC = {"cfg3": 272688384}  # round 2: mean DRAM read + write per launch over 7 captures (profiles/r2_ncu_kernels.json)
 
 
 # ---------------------------------------------------------------- our arm
