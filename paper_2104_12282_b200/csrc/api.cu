@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for profilers
+
 #include "../../include/tomo.h"
 #include "tomo_internal.h"
 
@@ -109,6 +111,12 @@ struct tomo_ctx {
 };
 
 namespace {
+
+// NVTX range for the duration of a C-ABI call (ncu --nvtx --nvtx-include "tomo_solve/" ...)
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
 
 int fail(tomo_ctx* c, int code, const std::string& msg) {
   if (c) c->err = msg;
@@ -796,6 +804,7 @@ int pcg_internal(tomo_ctx* c, double tol, int max_iters, tomo_solve_info* info) 
 // ====================================================================== operator / solve
 extern "C" int tomo_apply(tomo_ctx* c, const double* d_rho, int64_t n_e, const double* d_u,
                           double* d_y, int64_t n_dof) {
+  Range nvtx_range("tomo_apply");
   if (int rc = need_bound(c)) return rc;
   if (n_e != c->g.ne || n_dof != c->g.ndof) return fail(c, TOMO_ESIZE, "length mismatch (SPEC.md l.127)");
   if (!check_ptr(d_rho) || !check_ptr(d_u) || !check_ptr(d_y)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
@@ -809,6 +818,7 @@ extern "C" int tomo_apply(tomo_ctx* c, const double* d_rho, int64_t n_e, const d
 
 extern "C" int tomo_solve(tomo_ctx* c, const double* d_rho, int64_t n_e, double* d_u,
                           int64_t n_dof, double tol, int max_iters, tomo_solve_info* info) {
+  Range nvtx_range("tomo_solve");
   if (int rc = need_bound(c)) return rc;
   if (n_e != c->g.ne || n_dof != c->g.ndof) return fail(c, TOMO_ESIZE, "length mismatch (SPEC.md l.127)");
   if (!check_ptr(d_rho) || !check_ptr(d_u)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
@@ -840,6 +850,7 @@ extern "C" int tomo_compliance(tomo_ctx* c, const double* d_u, int64_t n_dof, do
 
 extern "C" int tomo_sensitivity(tomo_ctx* c, const double* d_rho, const double* d_u,
                                 double* d_dc, double* d_ce, double* energy_out) {
+  Range nvtx_range("tomo_sensitivity");
   if (int rc = need_bound(c)) return rc;
   if (!check_ptr(d_rho) || !check_ptr(d_u) || !check_ptr(d_dc) || (d_ce && !check_ptr(d_ce)))
     return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
@@ -854,6 +865,7 @@ extern "C" int tomo_sensitivity(tomo_ctx* c, const double* d_rho, const double* 
 
 extern "C" int tomo_filter(tomo_ctx* c, const double* d_in, double* d_out, int64_t n_e,
                            int transpose) {
+  Range nvtx_range("tomo_filter");
   if (int rc = need_bound(c)) return rc;
   if (n_e != c->g.ne) return fail(c, TOMO_ESIZE, "length mismatch");
   if (!check_ptr(d_in) || !check_ptr(d_out)) return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
@@ -877,6 +889,7 @@ extern "C" int tomo_volume_grad(tomo_ctx* c, double* d_dv, int64_t n_e) {
 extern "C" int tomo_oc_update(tomo_ctx* c, const double* d_x, const double* d_g,
                               const double* d_dv, int64_t n_e, double volfrac, double move,
                               double eta, double* d_xnew, double* lambda_out, int* steps_out) {
+  Range nvtx_range("tomo_oc_update");
   if (int rc = need_bound(c)) return rc;
   if (n_e != c->g.ne) return fail(c, TOMO_ESIZE, "length mismatch");
   if (!check_ptr(d_x) || !check_ptr(d_g) || !check_ptr(d_dv) || !check_ptr(d_xnew))
@@ -918,6 +931,7 @@ int evaluate_dev(tomo_ctx* c, const double* d_rho, double* d_u, double* d_dc, do
 extern "C" int tomo_evaluate(tomo_ctx* c, const double* d_rho, double* d_u, double* d_dc,
                              double* d_dcf, double tol, int max_iters, double* c_out,
                              tomo_solve_info* info) {
+  Range nvtx_range("tomo_evaluate");
   if (int rc = need_bound(c)) return rc;
   if (!check_ptr(d_rho) || !check_ptr(d_u) || !check_ptr(d_dcf) || (d_dc && !check_ptr(d_dc)))
     return fail(c, TOMO_EINVAL, "NULL or misaligned pointer");
@@ -927,6 +941,7 @@ extern "C" int tomo_evaluate(tomo_ctx* c, const double* d_rho, double* d_u, doub
 extern "C" int tomo_evaluate_host(tomo_ctx* c, const double* h_rho, double* h_u, double* h_dcf,
                                   double tol, int max_iters, double* c_out,
                                   tomo_solve_info* info) {
+  Range nvtx_range("tomo_evaluate_host");
   if (int rc = need_bound(c)) return rc;
   if (!h_rho || !h_dcf) return fail(c, TOMO_EINVAL, "NULL host pointer");
   const size_t be = sizeof(double) * (size_t)c->g.ne, bd = sizeof(double) * (size_t)c->g.ndof;
@@ -1305,6 +1320,7 @@ extern "C" int tomo_mg_bind(tomo_ctx* c, int levels, void* d_ws, size_t bytes) {
 
 extern "C" int tomo_solve_mg(tomo_ctx* c, const double* d_rho, int64_t n_e, double* d_u,
                              int64_t n_dof, double tol, int max_iters, tomo_solve_info* info) {
+  Range nvtx_range("tomo_solve_mg");
   if (int rc = need_bound(c)) return rc;
   if (!c->mg_bound) return fail(c, TOMO_ENOWORKSPACE, "call tomo_mg_bind first");
   if (n_e != c->g.ne || n_dof != c->g.ndof) return fail(c, TOMO_ESIZE, "length mismatch");
