@@ -955,7 +955,13 @@ __global__ void __launch_bounds__(256) k_filter(Grid g, const int* __restrict__ 
 // Weights wd2[|d|^2] live in registers (specialised tap sets) or shared memory (runtime M).
 // Per output: about (2R+1)(2R+2)/2 shared loads per input plane and one FMA per tap. Forward
 // mode multiplies the finished output by 1/Hs (P x = H x / Hs).
-constexpr int FT_X = 32, FT_Y = 8;  // output tile; ROWS output rows per thread (1 or 2)
+#ifndef TOMO_FT_ROWS
+#define TOMO_FT_ROWS 2  // output rows per thread for radii R <= 3 (A/B knob: 1, 2, 4)
+#endif
+#ifndef TOMO_FT_BLOCKS_PER_SM
+#define TOMO_FT_BLOCKS_PER_SM 3  // target resident blocks per SM when choosing z chunks
+#endif
+constexpr int FT_X = 32, FT_Y = 8;  // output tile; ROWS output rows per thread (1, 2 or 4)
 
 template <int R, int MM, int ROWS>
 __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const double* __restrict__ wd2, int M,
@@ -1375,16 +1381,17 @@ cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, 
   const int tiles = ((g.nx + FT_X - 1) / FT_X) * ((g.ny + FT_Y - 1) / FT_Y);
   // z chunks: aim at >= 3 blocks per SM, but no chunk thinner than 4R + 4 planes (the 2R
   // halo planes of a chunk cost FMAs)
-  int chunks = std::max(1, (3 * sms + tiles - 1) / tiles);
+  int chunks = std::max(1, (TOMO_FT_BLOCKS_PER_SM * sms + tiles - 1) / tiles);
   chunks = std::min(chunks, std::max(1, g.nz / (4 * R + 4)));
   const int zchunk = (g.nz + chunks - 1) / chunks;
   chunks = (g.nz + zchunk - 1) / zchunk;
   const dim3 grid(tiles * chunks);
   // two output rows per thread halve the shared loads per FMA where loads would bound (small
   // R); one row per thread for large R (FMA-bound, and the unrolled body stays in registers)
-#define TOMO_FT(RR, MMM)                                                                      \
-  k_filter_t<RR, MMM, (RR <= 3 ? 2 : 1)><<<grid, dim3(FT_X, FT_Y / (RR <= 3 ? 2 : 1)), 0, st>>>( \
-      g, wd2, M, iHs, in, out, transpose, zchunk)
+#define TOMO_FT(RR, MMM)                                                                  \
+  k_filter_t<RR, MMM, (RR <= 3 ? TOMO_FT_ROWS : 1)>                                         \
+      <<<grid, dim3(FT_X, FT_Y / (RR <= 3 ? TOMO_FT_ROWS : 1)), 0, st>>>(g, wd2, M, iHs, in, out, \
+                                                                     transpose, zchunk)
   if (R == 1 && M == 2) TOMO_FT(1, 2);
   else if (R == 1 && M == 3) TOMO_FT(1, 3);
   else if (R == 2 && M == 8) TOMO_FT(2, 8);

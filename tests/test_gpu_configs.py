@@ -182,7 +182,7 @@ def test_cfg1_loop_free_running_history():
     c = np.array(hist["c"])
     relc = np.abs(c - c_ref) / c_ref
     assert relc[0] <= 1e-9
-    assert np.max(relc) <= 1e-6, relc
+    assert np.max(relc) <= 1e-8, relc  # measured 3.3e-11 (profiles/r2_configs_report.json)
     assert c[-1] < c[0]  # the standard optimiser makes progress
     assert np.max(np.abs(cpu(hist["x_final"]) - xs["x50"])) <= 1e-4
 
