@@ -956,7 +956,10 @@ __global__ void __launch_bounds__(256) k_filter(Grid g, const int* __restrict__ 
 // Per output: about (2R+1)(2R+2)/2 shared loads per input plane and one FMA per tap. Forward
 // mode multiplies the finished output by 1/Hs (P x = H x / Hs).
 #ifndef TOMO_FT_ROWS
-#define TOMO_FT_ROWS 2  // output rows per thread for radii R <= 3 (A/B knob: 1, 2, 4)
+#define TOMO_FT_ROWS 1  // output rows per thread for radii R <= 3 (A/B knob: 1, 2, 4; 1 measured best)
+#endif
+#ifndef TOMO_FT_ZMIN_R
+#define TOMO_FT_ZMIN_R 4  // z chunks are at least ZMIN_R * R + 4 planes thick (halo FMA waste)
 #endif
 #ifndef TOMO_FT_BLOCKS_PER_SM
 #define TOMO_FT_BLOCKS_PER_SM 3  // target resident blocks per SM when choosing z chunks
@@ -1382,7 +1385,7 @@ cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, 
   // z chunks: aim at >= 3 blocks per SM, but no chunk thinner than 4R + 4 planes (the 2R
   // halo planes of a chunk cost FMAs)
   int chunks = std::max(1, (TOMO_FT_BLOCKS_PER_SM * sms + tiles - 1) / tiles);
-  chunks = std::min(chunks, std::max(1, g.nz / (4 * R + 4)));
+  chunks = std::min(chunks, std::max(1, g.nz / (TOMO_FT_ZMIN_R * R + 4)));
   const int zchunk = (g.nz + chunks - 1) / chunks;
   chunks = (g.nz + zchunk - 1) / zchunk;
   const dim3 grid(tiles * chunks);
