@@ -101,6 +101,7 @@ def test_filter_taps_bit_exact(lib, rmin, ntaps):
     (dict(nx=1, ny=1, nz=1, rmin=0.0), "rmin"), (dict(nx=1, ny=1, nz=1, h=-1.0), "h"),
     (dict(nx=1, ny=1, nz=1, bc=3, fixed=(2,), ldofs=(2,), lvals=(1.0,)), "load on fixed"),
     (dict(nx=1, ny=1, nz=1, bc=3, fixed=(24,)), "range"), (dict(nx=1, ny=1, nz=1, bc=9), "kind"),
+    (dict(nx=1024, ny=1024, nz=1024), "32-bit internal DOF index"),
 ])
 def test_create_validation(lib, kw, why):
     nx, ny, nz = kw.pop("nx"), kw.pop("ny"), kw.pop("nz")
@@ -128,6 +129,19 @@ def test_explicit_bc_merges_duplicate_loads(lib):
     v = (C.c_double * 4)()
     assert lib.tomo_get_load(hnd, d, v, C.byref(n)) == 0
     assert n.value == 2 and list(d[:2]) == [5, 8] and list(v[:2]) == [3.0, -1.0]
+    lib.tomo_destroy(hnd)
+
+
+def test_largest_grid_under_the_index_limit_is_accepted(lib):
+    """The maximum size: the internal (padded) DOF index is 32-bit, so the largest accepted
+    grid has 3 nnx_pad (ny+1) (nz+1) < 2^31 - 64 (890^3: 2.1e9 DOFs); its workspace still
+    fits a B200's HBM (183,359 MiB per nvidia-smi)."""
+    rc, hnd = _create(lib, 890, 890, 890)
+    assert rc == 0
+    assert lib.tomo_workspace_bytes(hnd) < 183359 * 1024 ** 2
+    lib.tomo_destroy(hnd)
+    rc, hnd = _create(lib, 900, 900, 900)
+    assert rc == -1
     lib.tomo_destroy(hnd)
 
 
