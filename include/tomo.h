@@ -192,8 +192,10 @@ int tomo_coarsen(tomo_ctx* fine, const double* d_z, int nb, double* d_zc, int64_
  * their BCs those of tomo_create_coarse(nb = 2). Preconditioner: one V-cycle with `nu`
  * damped-Jacobi sweeps (weight omega) before and after the coarse correction, full-weighting
  * restriction = transpose of trilinear prolongation, the coarsest level solved by the fused
- * Jacobi-PCG to coarse_tol (at most coarse_iters). Outer loop: flexible CG (Polak-Ribiere
- * beta) from x0 = 0, stopped on ||r_k|| <= tol ||f||; returns iterations >= 0 or a status.
+ * Jacobi-PCG to coarse_tol (at most coarse_iters launches). Outer loop: flexible CG
+ * (Polak-Ribiere beta) from x0 = 0 with its scalars on the device, stopped on ||r_k|| <= tol
+ * ||f||; the whole loop is one CUDA graph with a conditional WHILE node (host-batched
+ * iterations under tomo_set_graph(ctx, 0)); returns iterations >= 0 or a status.
  * tomo_mg_workspace_bytes is host-only (builds the level contexts); tomo_mg_bind binds a
  * caller-owned device workspace of that size (256-B aligned) on the context's stream.     */
 size_t tomo_mg_workspace_bytes(tomo_ctx* ctx, int levels);

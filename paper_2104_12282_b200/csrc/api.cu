@@ -68,7 +68,9 @@ struct tomo_ctx {
   std::vector<tomo_ctx*> mg;
   char* mg_ws = nullptr;
   size_t mg_off_U = 0, mg_off_R = 0, mg_off_P = 0, mg_off_Q = 0, mg_off_Z = 0, mg_off_Zo = 0,
-         mg_off_part = 0, mg_end = 0;
+         mg_off_part = 0, mg_off_fs = 0, mg_end = 0;
+  cudaGraph_t mg_graph = nullptr;        // WHILE(not done) { one flexible-CG iteration }
+  cudaGraphExec_t mg_exec = nullptr;
   std::vector<size_t> mg_level_off;
   OpArgs op_apply_P{}, op_apply_Z{};
   bool mg_bound = false;
@@ -459,6 +461,8 @@ extern "C" void tomo_destroy(tomo_ctx* c) {
   for (auto* l : c->mg) tomo_destroy(l);
   if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
   if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
+  if (c->mg_exec) cudaGraphExecDestroy(c->mg_exec);
+  if (c->mg_graph) cudaGraphDestroy(c->mg_graph);
   for (auto e : c->ev) cudaEventDestroy(e);
   delete c;
 }
@@ -1189,21 +1193,21 @@ int mg_build_maps(tomo_ctx* c) {
 
 double* mgv(tomo_ctx* c, size_t off) { return reinterpret_cast<double*>(c->mg_ws + off); }
 
-// PCG on context c with the right-hand side already in r(1) (padded): relative tolerance
-// tol on ||b||, from u = 0. The coarsest level of the V-cycle.
-int pcg_rhs(tomo_ctx* c, double tol, int max_iters, int* iters) {
+// Jacobi-PCG on context c with the right-hand side already in r(1) (padded): relative
+// tolerance tol on ||b||, from u = 0 - the coarsest level of the V-cycle. At most `launches`
+// fused PCG launches are issued without reading anything back (launches after convergence
+// exit at their first instruction): no host synchronisation, so the V-cycle can be captured
+// into a CUDA graph.
+int pcg_rhs_fixed(tomo_ctx* c, double tol, int launches) {
   const Grid& g = c->g;
   const size_t vb = sizeof(double) * (size_t)g.ndof_pad;
-  LAUNCH(c, launch_scal_init(c->scal(), 0.0, max_iters, c->st));
+  LAUNCH(c, launch_scal_init(c->scal(), 0.0, launches, c->st));
   LAUNCH(c, launch_norm2(g, c->r(1), c->scal(), c->part(), c->nb_b, c->st));
   LAUNCH(c, launch_set_tol(c->scal(), tol, c->st));
   CK(c, cudaMemsetAsync(c->u(), 0, vb, c->st));
   CK(c, cudaMemsetAsync(c->q(1), 0, vb, c->st));
   CK(c, cudaMemsetAsync(c->p(1), 0, vb, c->st));
-  Scal hs{};
-  if (int rc = run_pcg_loop(c, max_iters, &hs)) return rc;
-  if (hs.done == 3 && hs.status != TOMO_EBREAKDOWN) return fail(c, hs.status ? hs.status : TOMO_ENAN, "NaN in the coarse solve");
-  if (iters) *iters = hs.iters;
+  for (int k = 0; k <= launches; ++k) LAUNCH(c, launch_op(OP_PCG, c->op_pcg[k & 1], c->op_blocks, c->st));
   return TOMO_OK;
 }
 
@@ -1215,8 +1219,7 @@ int mg_vcycle(tomo_ctx* f, int l, const double* b, double* x) {
   const size_t vb = sizeof(double) * (size_t)g.ndof_pad;
   if (l == L - 1) {  // coarsest: approximate solve by Jacobi-PCG
     if (b != c->r(1)) CK(c, cudaMemcpyAsync(c->r(1), b, vb, cudaMemcpyDeviceToDevice, c->st));
-    int it = 0;
-    if (int rc = pcg_rhs(c, f->mg_coarse_tol, f->mg_coarse_iters, &it)) return rc;
+    if (int rc = pcg_rhs_fixed(c, f->mg_coarse_tol, f->mg_coarse_iters)) return rc;
     if (x != c->u()) CK(c, cudaMemcpyAsync(x, c->u(), vb, cudaMemcpyDeviceToDevice, c->st));
     return TOMO_OK;
   }
@@ -1242,22 +1245,6 @@ int mg_vcycle(tomo_ctx* f, int l, const double* b, double* x) {
   for (int s = 0; s < f->mg_nu; ++s) {
     LAUNCH(c, launch_op(OP_APPLY, ax, c->ap_blocks, c->st));
     LAUNCH(c, launch_jacobi_smooth(g, om, b, c->q(0), c->dinv(), c->dmask(), x, c->st));
-  }
-  return TOMO_OK;
-}
-
-// host sum of the dot3 block partials in block order (deterministic)
-int mg_dot3(tomo_ctx* f, const double* a, const double* b, const double* c3, double out[3]) {
-  const int nb = f->sms * 4;
-  LAUNCH(f, launch_dot3(f->g.ndof_pad, a, b, c3, mgv(f, f->mg_off_part), nb, f->st));
-  std::vector<double> h((size_t)3 * nb);
-  CK(f, cudaMemcpyAsync(h.data(), mgv(f, f->mg_off_part), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, f->st));
-  CK(f, cudaStreamSynchronize(f->st));
-  out[0] = out[1] = out[2] = 0.0;
-  for (int i = 0; i < nb; ++i) {
-    out[0] += h[3 * i];
-    out[1] += h[3 * i + 1];
-    out[2] += h[3 * i + 2];
   }
   return TOMO_OK;
 }
@@ -1297,6 +1284,7 @@ extern "C" size_t tomo_mg_workspace_bytes(tomo_ctx* c, int levels) {
   c->mg_off_Z = o; o = align_up(o + vp);
   c->mg_off_Zo = o; o = align_up(o + vp);
   c->mg_off_part = o; o = align_up(o + sizeof(double) * 3 * 4 * 1024);
+  c->mg_off_fs = o; o = align_up(o + sizeof(FcgScal));
   c->mg_end = o;
   return o;
 }
@@ -1314,6 +1302,8 @@ extern "C" int tomo_mg_bind(tomo_ctx* c, int levels, void* d_ws, size_t bytes) {
       return fail(c, rc, std::string("binding MG level: ") + tomo_last_error(c->mg[l]));
   }
   if (int rc = mg_build_maps(c)) return rc;
+  if (c->mg_exec) { cudaGraphExecDestroy(c->mg_exec); c->mg_exec = nullptr; }
+  if (c->mg_graph) { cudaGraphDestroy(c->mg_graph); c->mg_graph = nullptr; }
   c->mg_bound = true;
   return TOMO_OK;
 }
@@ -1344,36 +1334,70 @@ extern "C" int tomo_solve_mg(tomo_ctx* c, const double* d_rho, int64_t n_e, doub
   }
   double *U = mgv(c, c->mg_off_U), *R = mgv(c, c->mg_off_R), *Pv = mgv(c, c->mg_off_P),
          *Q = mgv(c, c->mg_off_Q), *Z = mgv(c, c->mg_off_Z), *Zo = mgv(c, c->mg_off_Zo);
-  // x0 = 0, r0 = f (the flexible CG below runs from a cold start, reading A12)
+  FcgScal* fs = reinterpret_cast<FcgScal*>(c->mg_ws + c->mg_off_fs);
+  double* part = mgv(c, c->mg_off_part);
+  const int nb = std::min(c->sms * 4, 4 * 1024);
+  // x0 = 0, r0 = f (the flexible CG runs from a cold start, reading A12); scalars on the device
   CK(c, cudaMemsetAsync(U, 0, vb, c->st));
   CK(c, cudaMemsetAsync(c->q(0), 0, vb, c->st));
   LAUNCH(c, launch_resid(g, c->q(0), R, c->ldp(), c->lv(), (int)c->load_dofs.size(), c->st));
   if (int rc = mg_vcycle(c, 0, R, Z)) return rc;
   CK(c, cudaMemcpyAsync(Pv, Z, vb, cudaMemcpyDeviceToDevice, c->st));
-  double d[3];
-  if (int rc = mg_dot3(c, R, Z, nullptr, d)) return rc;
-  double rz = d[0], rr = d[2];
-  const double stop = tol * c->fnorm;
-  int k = 0;
-  bool conv = std::sqrt(rr) <= stop;
-  while (!conv && k < max_iters) {
-    LAUNCH(c, launch_op(OP_APPLY, c->op_apply_P, c->ap_blocks, c->st));  // Q = K P
-    if (int rc = mg_dot3(c, Pv, Q, nullptr, d)) return rc;
-    const double pq = d[0];
-    if (!(pq > 0.0) || !std::isfinite(pq)) return fail(c, std::isnan(pq) ? TOMO_ENAN : TOMO_EBREAKDOWN, "MG-CG breakdown: p^T K p <= 0");
-    const double alpha = rz / pq;
-    LAUNCH(c, launch_axpy2(n, alpha, Pv, U, -alpha, Q, R, c->st));  // U += a P ; R -= a Q
-    ++k;
+  LAUNCH(c, launch_fcg_init(fs, tol * c->fnorm, max_iters, c->st));
+  LAUNCH(c, launch_fcg_dot(n, R, Z, nullptr, part, nb, fs, FCG_INIT, 0, c->st));
+  // one outer iteration: Q = K P, alpha, U/R update, Z = V-cycle(R), beta + stop test, P update
+  auto iteration = [&](unsigned long long cond) -> int {
+    LAUNCH(c, launch_op(OP_APPLY, c->op_apply_P, c->ap_blocks, c->st));
+    LAUNCH(c, launch_fcg_dot(n, Pv, Q, nullptr, part, nb, fs, FCG_ALPHA, 0, c->st));
+    LAUNCH(c, launch_fcg_axpy2(n, fs, Pv, U, Q, R, c->st));
     CK(c, cudaMemcpyAsync(Zo, Z, vb, cudaMemcpyDeviceToDevice, c->st));
     if (int rc = mg_vcycle(c, 0, R, Z)) return rc;
-    if (int rc = mg_dot3(c, R, Z, Zo, d)) return rc;  // r.z, r.z_old, r.r
-    rr = d[2];
-    if (!std::isfinite(rr)) return fail(c, TOMO_ENAN, "NaN/Inf in MG-CG");
-    if (std::sqrt(rr) <= stop) { conv = true; break; }
-    const double beta = (d[0] - d[1]) / rz;  // flexible (Polak-Ribiere) beta
-    rz = d[0];
-    LAUNCH(c, launch_xpby(n, Z, beta, Pv, c->st));  // P = Z + beta P
+    LAUNCH(c, launch_fcg_dot(n, R, Z, Zo, part, nb, fs, FCG_BETA, cond, c->st));
+    LAUNCH(c, launch_fcg_xpby(n, fs, Z, Pv, c->st));
+    return TOMO_OK;
+  };
+  FcgScal hf{};
+  if (c->use_graph) {
+    // the whole loop as one graph: a conditional WHILE node whose body is one iteration,
+    // captured from the stream; the beta/stop reduction clears the condition
+    if (!c->mg_exec) {
+      CK(c, cudaGraphCreate(&c->mg_graph, 0));
+      cudaGraphConditionalHandle h;
+      CK(c, cudaGraphConditionalHandleCreate(&h, c->mg_graph, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t cnode;
+      CK(c, cudaGraphAddNode(&cnode, c->mg_graph, nullptr, 0, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      CK(c, cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      const int rc = iteration(h);
+      cudaGraph_t captured = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(c->st, &captured);
+      if (rc) return rc;
+      CK(c, ec);
+      CK(c, cudaGraphInstantiate(&c->mg_exec, c->mg_graph, 0));
+    }
+    CK(c, cudaGraphLaunch(c->mg_exec, c->st));
+    CK(c, cudaMemcpyAsync(&hf, fs, sizeof(hf), cudaMemcpyDeviceToHost, c->st));
+    CK(c, cudaStreamSynchronize(c->st));
+  } else {
+    for (;;) {  // host-batched iterations, the scalars read back every 8
+      for (int i = 0; i < 8; ++i)
+        if (int rc = iteration(0)) return rc;
+      CK(c, cudaMemcpyAsync(&hf, fs, sizeof(hf), cudaMemcpyDeviceToHost, c->st));
+      CK(c, cudaStreamSynchronize(c->st));
+      if (hf.done) break;
+    }
   }
+  if (hf.done == 3)
+    return fail(c, hf.status ? hf.status : TOMO_EBREAKDOWN,
+                hf.status == TOMO_ENAN ? "NaN/Inf in MG-CG" : "MG-CG breakdown: p^T K p <= 0");
+  const int k = hf.k;
+  const bool conv = hf.done == 1;
+  const double rr = hf.rr, stop = tol * c->fnorm;
   // true residual, then u out
   CK(c, cudaMemcpyAsync(c->u(), U, vb, cudaMemcpyDeviceToDevice, c->st));
   LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->ap_blocks, c->st));
@@ -1394,6 +1418,8 @@ extern "C" int tomo_solve_mg(tomo_ctx* c, const double* d_rho, int64_t n_e, doub
 
 extern "C" int tomo_mg_params(tomo_ctx* c, int nu, double omega, int coarse_iters, double coarse_tol) {
   if (!c || nu < 1 || !(omega > 0 && omega < 2) || coarse_iters < 1 || !(coarse_tol > 0)) return TOMO_EINVAL;
+  if (c->mg_exec) { cudaGraphExecDestroy(c->mg_exec); c->mg_exec = nullptr; }
+  if (c->mg_graph) { cudaGraphDestroy(c->mg_graph); c->mg_graph = nullptr; }
   c->mg_nu = nu;
   c->mg_omega = omega;
   c->mg_coarse_iters = coarse_iters;

@@ -145,54 +145,6 @@ __global__ void k_coarsen_E(Grid gf, Grid gc, const double* __restrict__ Ef, dou
 }
 
 // ---- flexible-CG vector kernels (flat over padded vectors; pads are 0) -----------------
-__global__ void k_axpy2(long long n, double a, const double* __restrict__ x, double* __restrict__ y,
-                        double b, const double* __restrict__ z, double* __restrict__ w) {
-  // y += a x ; w += b z
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride) {
-    y[d] = fma(a, x[d], y[d]);
-    w[d] = fma(b, z[d], w[d]);
-  }
-}
-__global__ void k_xpby(long long n, const double* __restrict__ x, double b, double* __restrict__ y) {
-  // y = x + b y
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride)
-    y[d] = fma(b, y[d], x[d]);
-}
-
-// three dot products <a,b>, <a,c>, <a,a> in one pass: deterministic block partials
-__global__ void __launch_bounds__(256) k_dot3(long long n, const double* __restrict__ a,
-                                              const double* __restrict__ b,
-                                              const double* __restrict__ c, double* partials) {
-  __shared__ double red[3][8];
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride) {
-    const double av = a[d];
-    s0 = fma(av, b[d], s0);
-    s1 = c ? fma(av, c[d], s1) : 0.0;
-    s2 = fma(av, av, s2);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    red[0][threadIdx.x >> 5] = s0;
-    red[1][threadIdx.x >> 5] = s1;
-    red[2][threadIdx.x >> 5] = s2;
-  }
-  __syncthreads();
-  if (threadIdx.x < 3) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
-    partials[3 * blockIdx.x + threadIdx.x] = t;
-  }
-}
-
 }  // namespace
 
 cudaError_t launch_jacobi_smooth(const Grid& g, double omega, const double* b, const double* kx,
@@ -220,18 +172,148 @@ cudaError_t launch_coarsen_E(const Grid& gf, const Grid& gc, const double* Ef, d
   k_coarsen_E<<<nblk(gc.ne, 256, 148 * 16), 256, 0, st>>>(gf, gc, Ef, Ec, mode);
   return cudaGetLastError();
 }
-cudaError_t launch_axpy2(long long n, double a, const double* x, double* y, double b,
-                         const double* z, double* w, cudaStream_t st) {
-  k_axpy2<<<nblk(n, 256, 148 * 8), 256, 0, st>>>(n, a, x, y, b, z, w);
+
+namespace {
+// ---------------------------------------------------------------- device-resident flexible CG
+// The MG-preconditioned flexible CG with its scalars on the device (no host round trip per
+// iteration), so that a whole outer iteration can be captured into a CUDA graph.
+// k_fcg_dot: block partials of up to three dots of one pass; the last block sums them in
+// block order (deterministic) and applies the step `mode`:
+//   FCG_INIT  (a = R, b = Z):       rz = R.Z, rr = R.R; done if ||R|| <= stop
+//   FCG_ALPHA (a = P, b = Q):       alpha = rz / P.Q  (breakdown / NaN -> done = 3)
+//   FCG_BETA  (a = R, b = Z, c = Zo): rr = R.R; done = 1 if ||R|| <= stop, = 2 at max_iters;
+//                                   else beta = (R.Z - R.Zo) / rz (Polak-Ribiere), rz = R.Z
+// and clears the graph's WHILE condition when done. Every kernel of the iteration returns at
+// once when `done` is set.
+__device__ __forceinline__ double fcg_warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_fcg_dot(long long n, const double* __restrict__ a,
+                                                 const double* __restrict__ b,
+                                                 const double* __restrict__ c, double* partials,
+                                                 FcgScal* s, int mode, unsigned long long cond) {
+  __shared__ double red[3][8];
+  __shared__ int last;
+  if (mode != FCG_INIT && *(volatile int*)&s->done) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride) {
+    const double av = a[d];
+    s0 = fma(av, b[d], s0);
+    if (c) s1 = fma(av, c[d], s1);
+    s2 = fma(av, av, s2);
+  }
+  s0 = fcg_warp_sum(s0);
+  s1 = fcg_warp_sum(s1);
+  s2 = fcg_warp_sum(s2);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { red[0][w] = s0; red[1][w] = s1; red[2][w] = s2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { t0 += red[0][i]; t1 += red[1][i]; t2 += red[2][i]; }
+    partials[3 * blockIdx.x] = t0;
+    partials[3 * blockIdx.x + 1] = t1;
+    partials[3 * blockIdx.x + 2] = t2;
+    __threadfence();
+    last = atomicAdd(&s->cnt, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+  for (unsigned i = 0; i < gridDim.x; ++i) {
+    d0 += __ldcg(partials + 3 * i);
+    d1 += __ldcg(partials + 3 * i + 1);
+    d2 += __ldcg(partials + 3 * i + 2);
+  }
+  s->cnt = 0;
+  if (mode == FCG_INIT) {
+    s->rz = d0;
+    s->rr = d2;
+    s->k = 0;
+    s->done = sqrt(d2) <= s->stop ? 1 : 0;
+  } else if (mode == FCG_ALPHA) {
+    if (!(d0 > 0.0) || !isfinite(d0)) {
+      s->done = 3;
+      s->status = isnan(d0) ? -6 : -4;  // TOMO_ENAN / TOMO_EBREAKDOWN
+    } else {
+      s->alpha = s->rz / d0;
+    }
+  } else {
+    s->k += 1;
+    s->rr = d2;
+    if (!isfinite(d2)) {
+      s->done = 3;
+      s->status = -6;
+    } else if (sqrt(d2) <= s->stop) {
+      s->done = 1;
+    } else if (s->k >= s->max_iters) {
+      s->done = 2;
+    } else {
+      s->beta = (d0 - d1) / s->rz;
+      s->rz = d0;
+    }
+  }
+  __threadfence();
+  if (cond && s->done) cudaGraphSetConditional(cond, 0u);
+}
+
+// U += alpha P ; R -= alpha Q (alpha from the device scalars)
+__global__ void k_fcg_axpy2(long long n, const FcgScal* s, const double* __restrict__ P,
+                            double* __restrict__ U, const double* __restrict__ Q,
+                            double* __restrict__ R) {
+  if (*(volatile const int*)&s->done) return;
+  const double a = s->alpha;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride) {
+    U[d] = fma(a, P[d], U[d]);
+    R[d] = fma(-a, Q[d], R[d]);
+  }
+}
+
+// P = Z + beta P
+__global__ void k_fcg_xpby(long long n, const FcgScal* s, const double* __restrict__ Z,
+                           double* __restrict__ P) {
+  if (*(volatile const int*)&s->done) return;
+  const double b = s->beta;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n; d += stride)
+    P[d] = fma(b, P[d], Z[d]);
+}
+
+__global__ void k_fcg_init(FcgScal* s, double stop, int max_iters) {
+  s->rz = s->rr = s->alpha = s->beta = 0.0;
+  s->stop = stop;
+  s->k = 0;
+  s->done = 0;
+  s->status = 0;
+  s->max_iters = max_iters;
+  s->cnt = 0;
+}
+
+}  // namespace
+
+cudaError_t launch_fcg_dot(long long n, const double* a, const double* b, const double* c,
+                           double* partials, int nblocks, FcgScal* s, int mode,
+                           unsigned long long cond, cudaStream_t st) {
+  k_fcg_dot<<<nblocks, 256, 0, st>>>(n, a, b, c, partials, s, mode, cond);
   return cudaGetLastError();
 }
-cudaError_t launch_xpby(long long n, const double* x, double b, double* y, cudaStream_t st) {
-  k_xpby<<<nblk(n, 256, 148 * 8), 256, 0, st>>>(n, x, b, y);
+cudaError_t launch_fcg_axpy2(long long n, const FcgScal* s, const double* P, double* U,
+                             const double* Q, double* R, cudaStream_t st) {
+  k_fcg_axpy2<<<nblk(n, 256, 148 * 8), 256, 0, st>>>(n, s, P, U, Q, R);
   return cudaGetLastError();
 }
-cudaError_t launch_dot3(long long n, const double* a, const double* b, const double* c,
-                        double* partials, int nblocks, cudaStream_t st) {
-  k_dot3<<<nblocks, 256, 0, st>>>(n, a, b, c, partials);
+cudaError_t launch_fcg_xpby(long long n, const FcgScal* s, const double* Z, double* P,
+                            cudaStream_t st) {
+  k_fcg_xpby<<<nblk(n, 256, 148 * 8), 256, 0, st>>>(n, s, Z, P);
+  return cudaGetLastError();
+}
+cudaError_t launch_fcg_init(FcgScal* s, double stop, int max_iters, cudaStream_t st) {
+  k_fcg_init<<<1, 1, 0, st>>>(s, stop, max_iters);
   return cudaGetLastError();
 }
 

@@ -94,6 +94,15 @@ struct Scal {
   double* hist;       // optional device buffer: hist[k] = r_k^T r_k of launch k (tomo_set_history)
 };
 
+// Device scalars of the MG-preconditioned flexible CG (mg.cu k_fcg_*; api.cu tomo_solve_mg)
+struct FcgScal {
+  double rz, rr, alpha, beta, stop;
+  int k, done, status, max_iters;  // done: 0 running, 1 converged, 2 max_iters, 3 error
+  unsigned cnt;                    // last-block counter
+  int pad;
+};
+enum FcgMode { FCG_INIT = 0, FCG_ALPHA = 1, FCG_BETA = 2 };
+
 enum OpMode { OP_APPLY = 0, OP_PCG = 1 };
 
 // Operator tile: 32 x OP_BY threads. Warp w stages node rows w and w+1 of the tile (OP_BY+1
@@ -223,10 +232,14 @@ cudaError_t launch_prolong_add(const Grid& gf, const Grid& gc, const double* xc,
                                const uint8_t* maskf, double* xf, cudaStream_t st);
 cudaError_t launch_coarsen_E(const Grid& gf, const Grid& gc, const double* Ef, double* Ec,
                              int mode, cudaStream_t st);
-cudaError_t launch_axpy2(long long n, double a, const double* x, double* y, double b,
-                         const double* z, double* w, cudaStream_t st);
-cudaError_t launch_xpby(long long n, const double* x, double b, double* y, cudaStream_t st);
-cudaError_t launch_dot3(long long n, const double* a, const double* b, const double* c,
-                        double* partials, int nblocks, cudaStream_t st);
+
+cudaError_t launch_fcg_dot(long long n, const double* a, const double* b, const double* c,
+                           double* partials, int nblocks, FcgScal* s, int mode,
+                           unsigned long long cond, cudaStream_t st);
+cudaError_t launch_fcg_axpy2(long long n, const FcgScal* s, const double* P, double* U,
+                             const double* Q, double* R, cudaStream_t st);
+cudaError_t launch_fcg_xpby(long long n, const FcgScal* s, const double* Z, double* P,
+                            cudaStream_t st);
+cudaError_t launch_fcg_init(FcgScal* s, double stop, int max_iters, cudaStream_t st);
 
 }  // namespace tomo
