@@ -1372,10 +1372,23 @@ extern "C" int tomo_solve_mg(tomo_ctx* c, const double* d_rho, int64_t n_e, doub
       cudaGraphNode_t cnode;
       CK(c, cudaGraphAddNode(&cnode, c->mg_graph, nullptr, 0, &cp));
       cudaGraph_t body = cp.conditional.phGraph_out[0];
-      CK(c, cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-      const int rc = iteration(h);
-      cudaGraph_t captured = nullptr;
-      const cudaError_t ec = cudaStreamEndCapture(c->st, &captured);
+      // capture on a private stream (the bound one may be the legacy default stream, which
+      // cannot capture); every level's launches are redirected to it meanwhile
+      cudaStream_t cs = nullptr;
+      CK(c, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      std::vector<tomo_ctx*> all{c};
+      for (auto* l : c->mg) all.push_back(l);
+      const cudaStream_t bound = c->st;
+      for (auto* x : all) x->st = cs;
+      cudaError_t ec = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+      int rc = TOMO_OK;
+      if (ec == cudaSuccess) {
+        rc = iteration(h);
+        cudaGraph_t captured = nullptr;
+        ec = cudaStreamEndCapture(cs, &captured);
+      }
+      for (auto* x : all) x->st = bound;
+      cudaStreamDestroy(cs);
       if (rc) return rc;
       CK(c, ec);
       CK(c, cudaGraphInstantiate(&c->mg_exec, c->mg_graph, 0));
