@@ -179,3 +179,31 @@ def test_coarse_context_loads_match_oracle_restriction(lib, dims, bc, nb):
     assert lib.tomo_create_coarse(C.byref(bad), fine, 7) == -1  # 7 divides none of the grids
     lib.tomo_destroy(coarse)
     lib.tomo_destroy(fine)
+
+
+def test_concurrent_create_is_thread_safe(lib):
+    """tomo_create from many threads at once (ctypes releases the GIL): every context gets its
+    own KE and passes its Walsh-pattern self-check (the basis-change scratch was a
+    shared static array)."""
+    import threading
+    nus = [0.05 + 0.4 * i / 63 for i in range(64)]
+    res = [None] * len(nus)
+
+    def work(i):
+        rc, hnd = _create(lib, 3, 2, 2, nu=nus[i])
+        buf = (C.c_double * 576)()
+        ok = rc == 0 and lib.tomo_get_ke(hnd, buf) == 0
+        res[i] = (ok, np.array(buf[:]).reshape(24, 24))
+        lib.tomo_destroy(hnd)
+
+    for _ in range(3):
+        th = [threading.Thread(target=work, args=(i,)) for i in range(len(nus))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for i, nu in enumerate(nus):
+            ok, KE = res[i]
+            assert ok, nu
+            ref = fem.element_stiffness(nu, 1.0)
+            assert np.max(np.abs(KE - ref)) <= 1e-14 * np.max(np.abs(ref))
