@@ -73,7 +73,7 @@ def test_cfg4_full_solve_parity(name, idx, variant):
           f"dc {ddc:.1e} (bar {bar_dc:.1e}), true res {info.rel_res_true:.2e}")
     assert abs(c10 - meta["c"]) <= 1e-9 * abs(meta["c"])
     assert du <= bar_u and ddc <= bar_dc
-    k_sp = meta.get("pcg_single_pass_iters_1e-10")
+    k_sp = meta.get("pcg_single_pass_iters_1e-10") or (meta["pcg_iters_1e-10"] if variant == "uniform" else None)
     if k_sp is not None and variant == "uniform":
         # well conditioned: the kernel's recurrence reproduces its CPU run; at the void-0.7
         # contrast the count is a property of the finite-precision trajectory and is only
