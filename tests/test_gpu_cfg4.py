@@ -1,7 +1,7 @@
 """configs[4] full-solve parity (32^3 and 64^3, void fraction 0.7 and uniform
-0.5, plus 128x64x64 uniform) through the C ABI against the ORACLE's tight solutions (its textbook Jacobi-PCG to
+0.5, plus 128x64x64 and 192x96x96 uniform) through the C ABI against the ORACLE's tight solutions (its textbook Jacobi-PCG to
 1e-12 from x0 = 0, tests/golden/cfg4*_solve.{json,npz} (32^3, full vectors) and
-cfg4*_sampled.json (64^3 and 128x64x64: c, norms, seeded samples), scripts/make_golden.py).
+cfg4*_sampled.json (64^3 and larger: c, norms, seeded samples), scripts/make_golden.py).
 
 Bars (reading A14): the GPU solves to 1e-10 as BASELINE.json states; c to 1e-9; u, dc to
 max(1e-8, 2 delta_floor), delta_floor = the oracle's OWN 1e-10 solution against its 1e-12
@@ -23,7 +23,8 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 CASES = [("cfg4a_uniform", 0, "uniform"), ("cfg4a_void07", 0, "void07"),
-         ("cfg4b_uniform", 1, "uniform"), ("cfg4c_uniform", 2, "uniform")]
+         ("cfg4b_uniform", 1, "uniform"), ("cfg4c_uniform", 2, "uniform"),
+         ("cfg4d_uniform", 3, "uniform")]
 
 
 def gpu(a):
