@@ -70,3 +70,37 @@ def neighbor_counts(nx, ny, nz, rmin):
     """Number of in-domain taps per element (integer; for bit-exact parity)."""
     H, _ = filter_matrices(nx, ny, nz, rmin)
     return np.diff(H.indptr).astype(np.int64)
+
+
+def hs_of(nx, ny, nz, rmin, elems):
+    """Hs_e = sum of the in-domain tap weights of element e, for the listed elements only
+    (same tap set and summation order as filter_matrices; for grids whose full H does not fit
+    in memory - the paper's 1551-tap radius on its 1.46M-element Mesh 3)."""
+    e = np.asarray(elems, dtype=np.int64)
+    i, j, k = e % nx, (e // nx) % ny, e // (nx * ny)
+    out = np.zeros(e.size)
+    for dx, dy, dz, w in taps(rmin):  # tap by tap, vectorised over the elements
+        ok = (i + dx >= 0) & (i + dx < nx) & (j + dy >= 0) & (j + dy < ny) & (k + dz >= 0) & (k + dz < nz)
+        out += np.where(ok, w, 0.0)
+    return out
+
+
+def filter_rows(nx, ny, nz, rmin, elems, x, transpose=False):
+    """(P x)_e or (P^T x)_e for the listed elements only, by the definitions of SPEC:220-233:
+    (P x)_e = sum_j w_ej x_j / Hs_e; (P^T v)_e = sum_i w_ie v_i / Hs_i over the in-domain taps
+    (w symmetric). Element by element (sampled parity at sizes where P cannot be formed)."""
+    t = taps(rmin)
+    out = np.empty(len(elems))
+    for q, e in enumerate(np.asarray(elems).tolist()):
+        i, j, k = e % nx, (e // nx) % ny, e // (nx * ny)
+        nb, wt = [], []
+        for dx, dy, dz, w in t:
+            if 0 <= i + dx < nx and 0 <= j + dy < ny and 0 <= k + dz < nz:
+                nb.append((i + dx) + nx * ((j + dy) + ny * (k + dz)))
+                wt.append(w)
+        nb, wt = np.array(nb), np.array(wt)
+        if transpose:
+            out[q] = float(np.sum(wt * x[nb] / hs_of(nx, ny, nz, rmin, nb)))
+        else:
+            out[q] = float(np.sum(wt * x[nb])) / hs_of(nx, ny, nz, rmin, [e])[0]
+    return out

@@ -177,3 +177,17 @@ def test_simp_loop_makes_progress():
     assert all(s > 0 for s in h["steps"][1:])
     xf = h["x_final"]
     assert abs(np.sum(op.P @ xf) - p.volfrac * p.n_elem) <= 1e-8 * p.n_elem
+
+
+def test_filter_rows_match_the_full_matrix():
+    """oracle.filt.filter_rows / hs_of (element-by-element P x, P^T v for grids too large for
+    the full matrix) agree with filter_matrix on a small grid, forward and transpose."""
+    nx, ny, nz, rmin = 9, 7, 6, 2.6
+    P = filt.filter_matrix(nx, ny, nz, rmin)
+    _, Hs = filt.filter_matrices(nx, ny, nz, rmin)
+    x = np.random.default_rng(3).uniform(0, 1, nx * ny * nz)
+    elems = np.arange(0, nx * ny * nz, 7)
+    assert np.allclose(filt.hs_of(nx, ny, nz, rmin, elems), Hs[elems], rtol=1e-14, atol=0)
+    assert np.allclose(filt.filter_rows(nx, ny, nz, rmin, elems, x), (P @ x)[elems], rtol=1e-13, atol=0)
+    assert np.allclose(filt.filter_rows(nx, ny, nz, rmin, elems, x, transpose=True), (P.T @ x)[elems],
+                       rtol=1e-13, atol=0)
