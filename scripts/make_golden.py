@@ -117,7 +117,7 @@ def cfg4(idx_variant, n_sample=4096, seed=44):
     rho = inputs.density_void07(p) if variant == "void07" else inputs.density_uniform(p, 0.5)
     name = f"cfg4{'abcde'[idx]}_{variant}"
     full = p.n_elem <= 40_000
-    meta, u, dc, dcf, _ = tight(name, rho=rho, p=p, store_full=full, use_csr=True)
+    meta, u, dc, dcf, _ = tight(name, rho=rho, p=p, store_full=full, use_csr=p.n_elem < 2_000_000)
     if not full:
         rng = np.random.default_rng(seed)
         idof = np.sort(rng.choice(u.size, n_sample, replace=False))
