@@ -829,40 +829,29 @@ __global__ void __launch_bounds__(256) k_sens(Grid g, Walsh W, const double* __r
   const int ipen = (penal == (double)(int)penal && penal >= 1.0 && penal <= 8.0) ? (int)penal : 0;
   double energy = 0.0;
   double Flo[12], Fhi[12];
-  // node-plane loads of this lane (rows j and j+1, masked), issued one plane ahead of use
-  struct NodeRows { double a0[3], a1[3]; };
-  auto load = [&](int k, NodeRows& L) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) L.a0[c] = L.a1[c] = 0.0;
-    if (node_ok && k <= g.nz) {
+  auto face = [&](int k, double (&F)[12]) {  // Walsh face of node plane k for element (i, j)
+    double a0[3] = {0.0, 0.0, 0.0}, a1[3] = {0.0, 0.0, 0.0};
+    if (node_ok) {
       const long long n0 = node_dense(g, in, j, k), n1 = node_dense(g, in, j + 1, k);
       TCHECK(n0 >= 0 && n1 < g.nn && k <= g.nz);
       const unsigned m0 = __ldg(mask + mask_index(g, in, j, k));
       const unsigned m1 = __ldg(mask + mask_index(g, in, j + 1, k));
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double v0 = __ldg(u + 3 * n0 + c), v1 = __ldg(u + 3 * n1 + c);
-        L.a0[c] = ((m0 >> c) & 1u) ? 0.0 : v0;
-        L.a1[c] = ((m1 >> c) & 1u) ? 0.0 : v1;
+        a0[c] = ((m0 >> c) & 1u) ? 0.0 : __ldg(u + 3 * n0 + c);
+        a1[c] = ((m1 >> c) & 1u) ? 0.0 : __ldg(u + 3 * n1 + c);
       }
     }
-  };
-  auto face = [&](const NodeRows& L, double (&F)[12]) {  // Walsh face for element (i, j)
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double b0 = __shfl_down_sync(0xffffffffu, L.a0[c], 1);
-      const double b1 = __shfl_down_sync(0xffffffffu, L.a1[c], 1);
-      face_from(L.a0[c], b0, L.a1[c], b1, F, c);
+      const double b0 = __shfl_down_sync(0xffffffffu, a0[c], 1);
+      const double b1 = __shfl_down_sync(0xffffffffu, a1[c], 1);
+      face_from(a0[c], b0, a1[c], b1, F, c);
     }
   };
-  NodeRows cur, nxt;
-  load(k0, cur);
-  load(k0 + 1, nxt);
-  face(cur, Flo);
+  face(k0, Flo);
   for (int k = k0; k < k1; ++k) {
-    cur = nxt;
-    if (k + 2 <= k1) load(k + 2, nxt);  // in flight during this element's arithmetic
-    face(cur, Fhi);
+    face(k + 1, Fhi);
     if (elem_ok) {
       const long long e = in + (long long)g.nx * (j + (long long)g.ny * k);
       const double ce = element_energy(Flo, Fhi, W);
