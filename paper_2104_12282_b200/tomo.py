@@ -118,7 +118,7 @@ def load_library(path: str = LIB_PATH):
         lib = C.CDLL(path)
         for name, res, args in _SIGS:
             if os.environ.get("TOMO_LIB_PATH") and not hasattr(lib, name):
-                continue  # A/B timing of an older build (scripts/build_variant.sh)
+                continue  # A/B timing of a variant build (scripts/build_variants.py)
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
