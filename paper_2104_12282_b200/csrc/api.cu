@@ -6,7 +6,9 @@
 // (padded) PCG vectors. The PCG driver launches one fused single-pass PCG kernel per
 // iteration (kernels.cu, k_op<OP_PCG>), either as one CUDA graph with a conditional WHILE
 // node (default) or in host batches (tomo_set_graph(ctx, 0)), and reads the device
-// scalars back once per graph launch / batch.
+// scalars back once per graph launch / batch. Consecutive PCG launches are chained by
+// programmatic dependent launch (graph edges / launch attribute): a launch's blocks are
+// scheduled while its predecessor finishes and wait inside for its completion.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -62,6 +64,8 @@ struct tomo_ctx {
   cudaGraph_t pcg_graph = nullptr;        // WHILE(not done) { launch even; launch odd }
   bool use_graph = true;                  // tomo_set_graph: graph (1) or host batches (0)
   bool exact_beta = false;                // tomo_set_pcg_exact_beta: textbook beta (extra pass)
+  bool pdl = true;                        // programmatic dependent launch between PCG launches
+  int body_launches = 2;                  // PCG launches per WHILE body of the graph
   cudaGraphExec_t pcg_exec = nullptr;
   // multigrid hierarchy (tomo_mg_*): levels 1..L-1 are coarse contexts bound to the caller's
   // MG workspace; the outer flexible-CG vectors of the fine level live there too
@@ -563,6 +567,22 @@ int build_pcg_graph(tomo_ctx* c) {
   a0.cond = h;
   a1.cond = h;
   cudaGraphNode_t n0, n1;
+  c->body_launches = 2;
+  if (c->pdl && !c->exact_beta) {
+    // U launches per body chained by programmatic edges: launch i+1's blocks are scheduled
+    // while launch i finishes (its last block's reduction, the kernel boundary) and wait in
+    // griddepcontrol.wait for its completion. A WHILE-iteration boundary is an ordinary
+    // dependency, so the body is unrolled; launches after the one that sets `done` exit at
+    // their first instructions.
+    const int U = 8;
+    cudaGraphNode_t prev = nullptr;
+    for (int i = 0; i < U; ++i) {
+      cudaGraphNode_t n;
+      CK(c, add_pcg_node_pdl(body, &n, prev, (i & 1) ? a1 : a0, c->op_blocks));
+      prev = n;
+    }
+    c->body_launches = U;
+  } else {
   CK(c, add_pcg_node(body, &n0, nullptr, 0, a0, c->op_blocks));
   if (c->exact_beta) {
     cudaGraphNode_t b0, b1;
@@ -571,6 +591,7 @@ int build_pcg_graph(tomo_ctx* c) {
     CK(c, add_beta_node(body, &b1, &n1, 1, c->g, c->r(1), c->q(1), c->dinv(), c->scal(), c->part(), c->nb_b));
   } else {
     CK(c, add_pcg_node(body, &n1, &n0, 1, a1, c->op_blocks));
+  }
   }
   CK(c, cudaGraphInstantiate(&c->pcg_exec, c->pcg_graph, 0));
   return TOMO_OK;
@@ -626,6 +647,7 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   c->ws_bytes = bytes;
   c->st = static_cast<cudaStream_t>(stream);
   if (std::getenv("TOMO_NO_GRAPH")) c->use_graph = false;  // A/B knob, same as tomo_set_graph(ctx, 0)
+  if (std::getenv("TOMO_NO_PDL")) c->pdl = false;           // A/B knob: plain launch-to-launch order
   const Grid& g = c->g;
   int dev = 0;
   CK(c, cudaGetDevice(&dev));
@@ -718,7 +740,8 @@ int run_pcg_loop(tomo_ctx* c, int max_iters, Scal* hs_out) {
     if (prof) CK(c, cudaEventRecord(c->ev[1], c->st));
     CK(c, cudaMemcpyAsync(&hs, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
     CK(c, cudaStreamSynchronize(c->st));
-    const int nodes = 2 * ((hs.iters + 2) / 2);  // kernel nodes executed (even/odd pairs)
+    const int U = c->body_launches;
+    const int nodes = U * ((hs.iters + U) / U);  // kernel nodes executed (whole bodies)
     c->launches += nodes;
     if (prof) {
       float ms = 0;
@@ -740,7 +763,8 @@ int run_pcg_loop(tomo_ctx* c, int max_iters, Scal* hs_out) {
     if (nb <= 0) break;
     for (int i = 0; i < nb; ++i) {
       if (prof && i < 256) CK(c, cudaEventRecord(c->ev[2 * i], c->st));
-      LAUNCH(c, launch_op(OP_PCG, c->op_pcg[(k + i) & 1], c->op_blocks, c->st));
+      LAUNCH(c, launch_op(OP_PCG, c->op_pcg[(k + i) & 1], c->op_blocks, c->st,
+                          c->pdl && !c->exact_beta && i > 0));
       if (c->exact_beta) {
         const int par = (k + i) & 1;
         LAUNCH(c, launch_beta(c->g, c->r(par), c->q(par), c->dinv(), c->scal(), c->part(), c->nb_b, c->st));

@@ -333,9 +333,21 @@ struct Carry {
   unsigned pm;         // output node: fixed bits
 };
 
+#ifdef TOMO_EXP_TIMELINE  // timing experiment only: per-block globaltimer stamps of PCG launches
+__device__ unsigned long long g_tl[2][4096][7];  // [launch parity][block]: entry, loop end, exit, smid
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
     k_op(const __grid_constant__ OpArgs a) {
+#ifdef TOMO_EXP_TIMELINE
+  const unsigned long long tl0 = gtimer();
+#endif
   using L = Lay<MODE>;
   constexpr int NS = L::ns, STAGE = L::stage;
   extern __shared__ __align__(128) double smem[];
@@ -351,6 +363,9 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
 
   double beta = 0.0, alpha_prev = 0.0;
   if (MODE == OP_PCG) {
+    // programmatic dependent launch: this grid may have been scheduled while the previous
+    // PCG launch was finishing; everything below reads its results (no-op without PDL)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (*(volatile int*)&a.s->done) return;
     beta = *(volatile double*)&a.s->beta;
     alpha_prev = *(volatile double*)&a.s->alpha;
@@ -590,6 +605,13 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   }
   __syncthreads();  // segment done: CD / GS / stages may be reused by the next segment
   }
+  // the next PCG launch may be scheduled now (it waits for this grid's completion before it
+  // reads anything): its blocks take the slots of blocks that have finished their planes
+  if (MODE == OP_PCG) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef TOMO_EXP_TIMELINE
+  const unsigned long long tl1 = gtimer();
+  const int tl_par = MODE == OP_PCG ? (*(volatile int*)&a.s->k) & 1 : 0;
+#endif
 
   if (MODE == OP_PCG) {
     const unsigned nb = gridDim.x;
@@ -645,6 +667,14 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
       }
     }
   }
+#ifdef TOMO_EXP_TIMELINE
+  if (MODE == OP_PCG && t == 0 && blockIdx.x < 4096) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    auto& G = g_tl[tl_par][blockIdx.x];
+    G[0] = tl0; G[1] = tl1; G[2] = gtimer(); G[3] = smid;
+  }
+#endif
 }
 
 // ------------------------------------------------------------------ solve-level reductions and vector kernels
@@ -1257,8 +1287,22 @@ static void op_attr() {
   done[dev] = true;
 }
 
-cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st) {
+cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st, bool pdl) {
   op_attr();
+  if (mode == OP_PCG && pdl) {
+    // programmatic dependent launch after the previous PCG launch on this stream
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblocks);
+    cfg.blockDim = dim3(TX, BY);
+    cfg.dynamicSmemBytes = op_smem(1);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_op<OP_PCG>, a);
+  }
   if (mode == OP_PCG) k_op<OP_PCG><<<nblocks, dim3(TX, BY), op_smem(1), st>>>(a);
   else k_op<OP_APPLY><<<nblocks, dim3(TX, BY), op_smem(0), st>>>(a);
   return cudaGetLastError();
@@ -1275,6 +1319,19 @@ cudaError_t add_pcg_node(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNo
   kp.sharedMemBytes = (unsigned)op_smem(1);
   kp.kernelParams = args;
   return cudaGraphAddKernelNode(node, g, deps, ndeps, &kp);
+}
+
+cudaError_t add_pcg_node_pdl(cudaGraph_t g, cudaGraphNode_t* node, cudaGraphNode_t prev,
+                             const OpArgs& a, int nblocks) {
+  cudaError_t e = add_pcg_node(g, node, nullptr, 0, a, nblocks);
+  if (e != cudaSuccess || !prev) return e;
+  // programmatic edge: the node may launch once every block of `prev` has triggered
+  // (griddepcontrol.launch_dependents after its planes); it waits for prev's completion
+  // (griddepcontrol.wait) before reading anything
+  cudaGraphEdgeData ed = {};
+  ed.from_port = cudaGraphKernelNodePortProgrammatic;
+  ed.type = cudaGraphDependencyTypeProgrammatic;
+  return cudaGraphAddDependencies_v2(g, &prev, node, &ed, 1);
 }
 
 int op_occupancy(int mode) {
@@ -1459,3 +1516,9 @@ cudaError_t launch_dfma(double* out, int blocks, int iters, cudaStream_t st) {
 }
 
 }  // namespace tomo
+
+#ifdef TOMO_EXP_TIMELINE  // timing experiment only: copy the per-block stamps of the last two PCG launches
+extern "C" int tomo_exp_timeline(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, tomo::g_tl, sizeof(tomo::g_tl));
+}
+#endif

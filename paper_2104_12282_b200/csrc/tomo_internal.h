@@ -171,10 +171,13 @@ struct OpArgs {
 int op_tiles(const Grid& g);
 size_t op_smem(int mode);
 int op_occupancy(int mode);
-cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st);
+cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st, bool pdl = false);
 // kernel node of one PCG launch (args copied into the node)
 cudaError_t add_pcg_node(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode_t* deps,
                          size_t ndeps, const OpArgs& a, int nblocks);
+// the same node after `prev` with a programmatic-dependent-launch edge (prev may be null)
+cudaError_t add_pcg_node_pdl(cudaGraph_t g, cudaGraphNode_t* node, cudaGraphNode_t prev,
+                             const OpArgs& a, int nblocks);
 cudaError_t launch_simp(const Grid& g, const double* rho, double* E, double E0, double Emin,
                         double penal, Scal* s, cudaStream_t st);
 cudaError_t launch_jacobi(const Grid& g, const double* E, double ke_diag, double* dinv,
