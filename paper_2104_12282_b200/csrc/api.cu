@@ -544,6 +544,9 @@ int build_op_args(tomo_ctx* c) {
 }
 }  // namespace
 
+#ifndef TOMO_PDL_UNROLL
+#define TOMO_PDL_UNROLL 16
+#endif
 namespace {
 // The whole PCG loop as one graph: a conditional WHILE node whose body is the even and the
 // odd launch; the last block of a launch that sets `done` clears the condition. Launches
@@ -574,7 +577,7 @@ int build_pcg_graph(tomo_ctx* c) {
     // griddepcontrol.wait for its completion. A WHILE-iteration boundary is an ordinary
     // dependency, so the body is unrolled; launches after the one that sets `done` exit at
     // their first instructions.
-    const int U = 8;
+    const int U = TOMO_PDL_UNROLL;
     cudaGraphNode_t prev = nullptr;
     for (int i = 0; i < U; ++i) {
       cudaGraphNode_t n;

@@ -147,8 +147,14 @@ __device__ __forceinline__ bool arrive_last(unsigned* cnt, unsigned nblocks, int
   const int t = threadIdx.x + blockDim.x * threadIdx.y;
   __syncthreads();
   if (t == 0) {
+#if TOMO_ACQREL_ARRIVE
+    // one acq_rel atomic: releases this block's partials, and the last block acquires all
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt) : "memory");
+#else
     __threadfence();
     unsigned prev = atomicAdd(cnt, 1u);
+#endif
     *s_flag = (prev == nblocks - 1);
   }
   __syncthreads();

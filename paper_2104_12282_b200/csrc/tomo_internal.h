@@ -140,6 +140,9 @@ constexpr int OP_GSREG_APPLY = TOMO_GSREG_APPLY, OP_GSREG_PCG = TOMO_GSREG_PCG;
 #define TOMO_PINGPONG_PCG 0
 #endif
 constexpr bool OP_PINGPONG_PCG = TOMO_PINGPONG_PCG != 0;
+#ifndef TOMO_ACQREL_ARRIVE
+#define TOMO_ACQREL_ARRIVE 0  // A/B: last-block arrival as one acq_rel atomic (kernels.cu arrive_last)
+#endif
 #ifndef TOMO_OP_NS_APPLY
 #define TOMO_OP_NS_APPLY 6
 #endif
