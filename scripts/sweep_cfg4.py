@@ -23,9 +23,9 @@ for idx in range(5):
     for variant in ("void07", "uniform"):
         rho_np = inputs.density_void07(p) if variant == "void07" else inputs.density_uniform(p, 0.5)
         rho = torch.tensor(rho_np, dtype=torch.float64, device="cuda:0")
-    # tomo_bench_apply applies the operator to the workspace's internal u: make it a realistic
-    # field (a 20-iteration PCG iterate) rather than the zeros left by tomo_bind
-    t.solve(rho, tol=0.0, max_iters=20)
+        # tomo_bench_apply applies the operator to the workspace's internal u: make it a
+        # realistic field (a 20-iteration PCG iterate) rather than the zeros left by tomo_bind
+        t.solve(rho, tol=0.0, max_iters=20)
         ms = t.bench_apply(rho, reps=100)
         # algorithmic bytes of K_hat u: read u, write y (8 B/DOF each), E (8 B/elem), mask (1 B/node)
         b = 16 * p.n_dof + 8 * p.n_elem + p.n_node
