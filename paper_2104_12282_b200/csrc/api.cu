@@ -699,7 +699,7 @@ int need_bound(tomo_ctx* c) {
 // gather kernel
 cudaError_t run_filter(tomo_ctx* c, const double* in, double* out, int transpose) {
   if (!std::getenv("TOMO_FILTER_GATHER")) {  // A/B knob: force the per-tap gather kernel
-    const cudaError_t e = launch_filter_tiled(c->g, c->filt_R, c->filt_M, c->wd2v(), c->iHs(), in, out,
+    const cudaError_t e = launch_filter_tiled(c->g, c->filt_R, c->filt_M, c->wd2v(), c->wd2.data(), c->iHs(), in, out,
                                               transpose, c->sms, c->st);
     if (e != cudaErrorNotSupported) return e;
   }

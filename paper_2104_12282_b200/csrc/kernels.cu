@@ -991,6 +991,9 @@ __global__ void __launch_bounds__(256) k_filter(Grid g, const int* __restrict__ 
 // Weights wd2[|d|^2] live in registers (specialised tap sets) or shared memory (runtime M).
 // Per output: about (2R+1)(2R+2)/2 shared loads per input plane and one FMA per tap. Forward
 // mode multiplies the finished output by 1/Hs (P x = H x / Hs).
+#ifndef TOMO_FT_SHELL
+#define TOMO_FT_SHELL 1  // specialised radii: shell sums (A/B knob: 0 = one FMA per tap)
+#endif
 #ifndef TOMO_FT_ROWS
 #define TOMO_FT_ROWS 1  // output rows per thread for radii R <= 3 (A/B knob: 1, 2, 4; 1 measured best)
 #endif
@@ -1002,8 +1005,31 @@ __global__ void __launch_bounds__(256) k_filter(Grid g, const int* __restrict__ 
 #endif
 constexpr int FT_X = 32, FT_Y = 8;  // output tile; ROWS output rows per thread (1, 2 or 4)
 
+// shell bookkeeping of the tiled filter (constant-folded once the tap loops are unrolled):
+// is (dx, dy) the first tap of its shell dx^2 + dy^2 in (dy, dx) order; has shell m a tap
+__host__ __device__ constexpr bool ft_first_in_shell(int dx, int dy, int R) {
+  for (int y = -R; y <= R; ++y)
+    for (int x = -R; x <= R; ++x) {
+      if (y == dy && x == dx) return true;
+      if (x * x + y * y == dx * dx + dy * dy) return false;
+    }
+  return true;
+}
+__host__ __device__ constexpr bool ft_shell_nonempty(int m, int R) {
+  for (int y = -R; y <= R; ++y)
+    for (int x = -R; x <= R; ++x)
+      if (x * x + y * y == m) return true;
+  return false;
+}
+
+// cone weights by |d|^2 as a by-value kernel parameter: constant-bank operands of the FMAs
+struct FtW {
+  double w[64];
+};
+
 template <int R, int MM, int ROWS>
-__global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const double* __restrict__ wd2, int M,
+__global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const __grid_constant__ FtW fw,
+                                                  const double* __restrict__ wd2, int M,
                                                   const double* __restrict__ iHs,
                                                   const double* __restrict__ in,
                                                   double* __restrict__ out, int transpose,
@@ -1019,8 +1045,8 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const d
   const int x0 = (tile % tiles_x) * FT_X, y0 = (tile / tiles_x) * FT_Y;
   const int z0 = ch * zchunk, z1 = min(g.nz, z0 + zchunk);
   const int Mr = MM >= 0 ? MM : M;
-  constexpr int WN = MM >= 0 ? MM + 1 : 1;
-  double w[WN];  // specialised tap sets: weights in registers
+  constexpr int WN = MM >= 0 && !(R <= 3 && TOMO_FT_SHELL) ? MM + 1 : 1;
+  double w[WN];  // specialised tap sets without shells: weights in registers
 #pragma unroll
   for (int d = 0; d < WN; ++d) w[d] = wd2[d];
   if (MM < 0)
@@ -1086,6 +1112,39 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const d
     double ih[ROWS];
     load_ih(zi - R, ih);
     const double* P = pl[b];
+    if constexpr (MM >= 0 && R <= 3 && TOMO_FT_SHELL) {
+      // shell sums: the weight depends on |d|^2 = m + dz^2 only, so the taps of one input
+      // plane are first summed over each 2-D shell m = dx^2 + dy^2 (one DADD per tap), and
+      // every output plane dz takes one FMA per shell (cfg3, rmin 3: 19 DADD + 24 DFMA per
+      // element and input plane instead of 93 DFMA: 25.1 -> 23.2 us). The loops unroll
+      // completely, so S[] indices are constants. Not for rmin 7.2: its ~30 live shell sums
+      // take the kernel to 204 registers and one block per SM (1323 vs 214 us measured).
+#pragma unroll
+      for (int h = 0; h < ROWS; ++h) {
+        double S[MM + 1];
+#pragma unroll
+        for (int dy = -R; dy <= R; ++dy) {
+#pragma unroll
+          for (int dx = -R; dx <= R; ++dx) {
+            const int m = dx * dx + dy * dy;
+            if (m > MM) continue;
+            TCHECK((ty + h * FT_YT + R + dy) * PX + tx + R + dx < PX * PY);
+            const double v = P[(ty + h * FT_YT + R + dy) * PX + tx + R + dx];
+            if (ft_first_in_shell(dx, dy, R)) S[m] = v;
+            else S[m] += v;
+          }
+        }
+#pragma unroll
+        for (int m = 0; m <= MM; ++m) {
+          if (!ft_shell_nonempty(m, R)) continue;
+#pragma unroll
+          for (int j = 0; j < NA; ++j) {
+            const int dz = R - j;
+            if (m + dz * dz <= MM) acc[h][j] = fma(fw.w[m + dz * dz], S[m], acc[h][j]);
+          }
+        }
+      }
+    } else {
 #pragma unroll
     for (int dy = -R; dy <= R + (ROWS - 1) * FT_YT; ++dy) {
 #pragma unroll
@@ -1115,6 +1174,7 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const d
           }
         }
       }
+    }
     }
     flush(zi - R, ih);
     if (zi + 1 == ze)  // drain: outputs whose remaining input planes lie outside the domain
@@ -1441,9 +1501,9 @@ cudaError_t launch_filter(const Grid& g, const int* taps, const double* w, int n
 // tiled filter launch for a ball of radius^2 M (R = floor(sqrt(M))): specialised tap sets of
 // the configs (rmin 1.5, 2, 3 and the paper's 7.2) and a runtime-M kernel per R up to 8;
 // returns cudaErrorNotSupported when R > 8 (the caller falls back to k_filter)
-cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, const double* iHs,
-                                const double* in, double* out, int transpose, int sms,
-                                cudaStream_t st) {
+cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, const double* hw,
+                                const double* iHs, const double* in, double* out, int transpose,
+                                int sms, cudaStream_t st) {
   const int tiles = ((g.nx + FT_X - 1) / FT_X) * ((g.ny + FT_Y - 1) / FT_Y);
   // z chunks: aim at >= 3 blocks per SM, but no chunk thinner than 4R + 4 planes (the 2R
   // halo planes of a chunk cost FMAs)
@@ -1454,9 +1514,11 @@ cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, 
   const dim3 grid(tiles * chunks);
   // two output rows per thread halve the shared loads per FMA where loads would bound (small
   // R); one row per thread for large R (FMA-bound, and the unrolled body stays in registers)
+  FtW fw{};
+  for (int d = 0; d <= M && d < 64; ++d) fw.w[d] = hw[d];
 #define TOMO_FT(RR, MMM)                                                                  \
   k_filter_t<RR, MMM, (RR <= 3 ? TOMO_FT_ROWS : 1)>                                         \
-      <<<grid, dim3(FT_X, FT_Y / (RR <= 3 ? TOMO_FT_ROWS : 1)), 0, st>>>(g, wd2, M, iHs, in, out, \
+      <<<grid, dim3(FT_X, FT_Y / (RR <= 3 ? TOMO_FT_ROWS : 1)), 0, st>>>(g, fw, wd2, M, iHs, in, out, \
                                                                      transpose, zchunk)
   if (R == 1 && M == 2) TOMO_FT(1, 2);
   else if (R == 1 && M == 3) TOMO_FT(1, 3);

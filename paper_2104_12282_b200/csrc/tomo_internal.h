@@ -212,9 +212,9 @@ cudaError_t launch_filter_sums(const Grid& g, const int* taps, const double* w, 
 cudaError_t launch_filter(const Grid& g, const int* taps, const double* w, int ntaps,
                           const double* Hs, const double* in, double* out, int transpose,
                           cudaStream_t st);
-cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, const double* iHs,
-                                const double* in, double* out, int transpose, int sms,
-                                cudaStream_t st);
+cudaError_t launch_filter_tiled(const Grid& g, int R, int M, const double* wd2, const double* hw,
+                                const double* iHs, const double* in, double* out, int transpose,
+                                int sms, cudaStream_t st);
 cudaError_t launch_oc(int ne, const double* x, const double* g, const double* dv,
                       double* xnew, double target, double move, double eta,
                       double* partials, double* out2, int grid_blocks, cudaStream_t st);
