@@ -484,6 +484,12 @@ extern "C" int tomo_sizes(const tomo_ctx* c, int64_t out[5]) {
 
 namespace {
 // operator launch variants: maps over the padded internal vectors
+// the PCG control in the separate one-block kernel k_pcg_red (with PDL, single-pass beta;
+// TOMO_NO_SEP_RED: the last block of each launch does it, as before)
+int pcg_sep(const tomo_ctx* c) {
+  return c->pdl && !c->exact_beta && !std::getenv("TOMO_NO_SEP_RED") ? 1 : 0;
+}
+
 int build_op_args(tomo_ctx* c) {
   const Grid& g = c->g;
   // row-SoA vectors: a 3-D map over (x, 3 * y + component, z), sub-row pitch 8 nnx_pad bytes
@@ -539,6 +545,7 @@ int build_op_args(tomo_ctx* c) {
     a.pnew = c->p(n);
     a.out = c->q(n);
     a.u = c->u();
+    a.sep = pcg_sep(c);
   }
   return TOMO_OK;
 }
@@ -577,12 +584,20 @@ int build_pcg_graph(tomo_ctx* c) {
     // griddepcontrol.wait for its completion. A WHILE-iteration boundary is an ordinary
     // dependency, so the body is unrolled; launches after the one that sets `done` exit at
     // their first instructions.
+    // With OpArgs::sep each PCG launch is followed by the one-block control kernel
+    // k_pcg_red (programmatic edges both ways): launch i+1 is scheduled once launch i is
+    // complete and issues its first TMA loads while k_pcg_red sums launch i's partials.
     const int U = TOMO_PDL_UNROLL;
     cudaGraphNode_t prev = nullptr;
     for (int i = 0; i < U; ++i) {
       cudaGraphNode_t n;
-      CK(c, add_pcg_node_pdl(body, &n, prev, (i & 1) ? a1 : a0, c->op_blocks));
+      const OpArgs& ai = (i & 1) ? a1 : a0;
+      CK(c, add_pcg_node_pdl(body, &n, prev, ai, c->op_blocks));
       prev = n;
+      if (ai.sep) {
+        CK(c, add_pcg_red_node(body, &n, prev, ai, c->op_blocks));
+        prev = n;
+      }
     }
     c->body_launches = U;
   } else {
@@ -744,7 +759,7 @@ int run_pcg_loop(tomo_ctx* c, int max_iters, Scal* hs_out) {
     CK(c, cudaMemcpyAsync(&hs, c->scal(), sizeof(Scal), cudaMemcpyDeviceToHost, c->st));
     CK(c, cudaStreamSynchronize(c->st));
     const int U = c->body_launches;
-    const int nodes = U * ((hs.iters + U) / U);  // kernel nodes executed (whole bodies)
+    const int nodes = U * ((hs.iters + U) / U) * (c->op_pcg[0].sep ? 2 : 1);  // whole bodies
     c->launches += nodes;
     if (prof) {
       float ms = 0;
@@ -768,6 +783,7 @@ int run_pcg_loop(tomo_ctx* c, int max_iters, Scal* hs_out) {
       if (prof && i < 256) CK(c, cudaEventRecord(c->ev[2 * i], c->st));
       LAUNCH(c, launch_op(OP_PCG, c->op_pcg[(k + i) & 1], c->op_blocks, c->st,
                           c->pdl && !c->exact_beta && i > 0));
+      if (c->op_pcg[0].sep) LAUNCH(c, launch_pcg_red(c->op_pcg[(k + i) & 1], c->op_blocks, c->st, true));
       if (c->exact_beta) {
         const int par = (k + i) & 1;
         LAUNCH(c, launch_beta(c->g, c->r(par), c->q(par), c->dinv(), c->scal(), c->part(), c->nb_b, c->st));
@@ -1089,6 +1105,7 @@ extern "C" int tomo_set_history(tomo_ctx* c, double* d_hist, int n) {
 extern "C" int tomo_set_pcg_exact_beta(tomo_ctx* c, int on) {
   if (!c) return TOMO_EINVAL;
   c->exact_beta = on != 0;
+  c->op_pcg[0].sep = c->op_pcg[1].sep = pcg_sep(c);
   if (c->bound) return build_pcg_graph(c);
   return TOMO_OK;
 }
@@ -1234,7 +1251,10 @@ int pcg_rhs_fixed(tomo_ctx* c, double tol, int launches) {
   CK(c, cudaMemsetAsync(c->u(), 0, vb, c->st));
   CK(c, cudaMemsetAsync(c->q(1), 0, vb, c->st));
   CK(c, cudaMemsetAsync(c->p(1), 0, vb, c->st));
-  for (int k = 0; k <= launches; ++k) LAUNCH(c, launch_op(OP_PCG, c->op_pcg[k & 1], c->op_blocks, c->st));
+  for (int k = 0; k <= launches; ++k) {
+    LAUNCH(c, launch_op(OP_PCG, c->op_pcg[k & 1], c->op_blocks, c->st));
+    if (c->op_pcg[0].sep) LAUNCH(c, launch_pcg_red(c->op_pcg[k & 1], c->op_blocks, c->st, false));
+  }
   return TOMO_OK;
 }
 

@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   const Grid& g = a.g;
 
   double beta = 0.0, alpha_prev = 0.0;
-  if (MODE == OP_PCG) {
+  if (MODE == OP_PCG && !a.sep) {
     // programmatic dependent launch: this grid may have been scheduled while the previous
     // PCG launch was finishing; everything below reads its results (no-op without PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -423,6 +423,21 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
     for (int s = 0; s < NS && it0 + s < nit; ++s)
       issue_plane<MODE>(a, stages + ((git + s) % NS) * STAGE, &bars[(git + s) % NS], org, i0, j0,
                         kbeg - 1 + it0 + s);
+  }
+  if (MODE == OP_PCG && a.sep && u0 - (kend - kbeg) == ub) {
+    // separate reduction (OpArgs::sep): this grid was scheduled after the previous PCG
+    // launch completed (the reduction kernel between them triggers it only then), so the
+    // loads above already read final data while that kernel sums the partials; its alpha,
+    // beta and stop flag are read once it has completed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (*(volatile int*)&a.s->done) {
+      if (t == 0)  // no bulk copy may be in flight at exit
+        for (int s = 0; s < NS && it0 + s < nit; ++s)
+          mbar_wait(&bars[(git + s) % NS], (unsigned)((git + s) / NS) & 1u);
+      return;
+    }
+    beta = *(volatile double*)&a.s->beta;
+    alpha_prev = *(volatile double*)&a.s->alpha;
   }
 
   // output node (i0-1+tx, j0+ty) = top node of this warp's element row
@@ -619,7 +634,11 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   const int tl_par = MODE == OP_PCG ? (*(volatile int*)&a.s->k) & 1 : 0;
 #endif
 
-  if (MODE == OP_PCG) {
+  if (MODE == OP_PCG && a.sep) {
+    // the grid totals, the stop test and alpha, beta are k_pcg_red's (the next kernel)
+    block_sum5(acc, red);
+    if (t < 5) a.partials[5 * blockIdx.x + t] = acc[t];
+  } else if (MODE == OP_PCG) {
     const unsigned nb = gridDim.x;
     const unsigned b = blockIdx.x;
     block_sum5(acc, red);
@@ -681,6 +700,63 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
     G[0] = tl0; G[1] = tl1; G[2] = gtimer(); G[3] = smid;
   }
 #endif
+}
+
+// The control of PCG iteration k in its own one-block kernel (OpArgs::sep): after launch k
+// of k_op<OP_PCG> has completed, sum its block partials in the fixed order of k_op's last
+// block (same thread count, same loop, same block_sum5: the same totals bit for bit), test
+// convergence / max_iters / breakdown / NaN and set alpha_k, beta_k - the same decision as
+// the last-block path. It lets launch k+1 be scheduled as soon as launch k is complete, so
+// launch k+1's first TMA loads overlap this reduction.
+__global__ void __launch_bounds__(NT) k_pcg_red(const double* __restrict__ partials, int nb, Scal* s,
+                                                unsigned long long cond) {
+  __shared__ double red[168];
+  asm volatile("griddepcontrol.wait;" ::: "memory");               // launch k complete
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // launch k+1 may start
+  if (*(volatile int*)&s->done) return;
+  const int t = threadIdx.x;
+  double tot[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (unsigned i = t; i < (unsigned)nb; i += NT) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) tot[q] += __ldcg(partials + 5 * (size_t)i + q);
+  }
+  block_sum5(tot, red);
+  if (t == 0) {
+    const int k = s->k;
+    const double pq = tot[0], rz = tot[1], rr = tot[2], zq = tot[3], qdq = tot[4];
+    s->pq = pq;
+    s->rz = rz;
+    s->rr = rr;
+    if (k < s->hist_n) s->hist[k] = rr;
+#ifdef TOMO_EXP_NOSTOP  // timing experiments: run exactly max_iters launches whatever the values
+    if (k >= s->max_iters) { s->done = 2; s->iters = k; } else { s->alpha = 0.5; s->beta = 0.5; s->k = k + 1; }
+    if (false) {
+#else
+    if (!isfinite(pq) || !isfinite(rz) || !isfinite(rr) || !isfinite(zq) || !isfinite(qdq)) {
+#endif
+      s->status = -6;  // TOMO_ENAN
+      s->done = 3;
+      s->iters = k;
+    } else if (sqrt(rr) <= s->tol_fnorm) {
+      s->done = 1;  // r_k converged: u_k (written by launch k) is the solution
+      s->iters = k;
+    } else if (k >= s->max_iters) {
+      s->done = 2;
+      s->iters = k;
+    } else if (!(pq > 0.0)) {
+      s->status = -4;  // TOMO_EBREAKDOWN
+      s->done = 3;
+      s->iters = k;
+    } else {
+      const double alpha = rz / pq;
+      const double rz_next = fma(alpha * alpha, qdq, fma(-2.0 * alpha, zq, rz));
+      s->alpha = alpha;
+      s->beta = rz_next / rz;
+      s->k = k + 1;
+    }
+    __threadfence();
+    if (cond && s->done) cudaGraphSetConditional(cond, 0u);  // end the graph's loop
+  }
 }
 
 // ------------------------------------------------------------------ solve-level reductions and vector kernels
@@ -1385,6 +1461,39 @@ cudaError_t add_pcg_node(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNo
   kp.sharedMemBytes = (unsigned)op_smem(1);
   kp.kernelParams = args;
   return cudaGraphAddKernelNode(node, g, deps, ndeps, &kp);
+}
+
+cudaError_t launch_pcg_red(const OpArgs& a, int nblocks, cudaStream_t st, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(NT);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_pcg_red, (const double*)a.partials, nblocks, a.s, 0ull);
+}
+
+cudaError_t add_pcg_red_node(cudaGraph_t g, cudaGraphNode_t* node, cudaGraphNode_t prev,
+                             const OpArgs& a, int nblocks) {
+  cudaKernelNodeParams kp = {};
+  const double* part = a.partials;
+  Scal* sc = a.s;
+  unsigned long long cond = a.cond;
+  void* args[] = {(void*)&part, &nblocks, &sc, &cond};
+  kp.func = reinterpret_cast<void*>(k_pcg_red);
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(NT);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  cudaError_t e = cudaGraphAddKernelNode(node, g, nullptr, 0, &kp);
+  if (e != cudaSuccess || !prev) return e;
+  cudaGraphEdgeData ed = {};
+  ed.from_port = cudaGraphKernelNodePortProgrammatic;
+  ed.type = cudaGraphDependencyTypeProgrammatic;
+  return cudaGraphAddDependencies_v2(g, &prev, node, &ed, 1);
 }
 
 cudaError_t add_pcg_node_pdl(cudaGraph_t g, cudaGraphNode_t* node, cudaGraphNode_t prev,

@@ -168,6 +168,7 @@ struct OpArgs {
   int ntiles;           // x-y tiles
   int zchunks;          // 0: persistent balanced schedule; > 0: block = (tile, z-chunk)
   unsigned long long cond;  // PCG in a CUDA graph: WHILE-node handle cleared when done (0: none)
+  int sep;              // PCG: 1 = the grid reduction / control runs in k_pcg_red after each launch
 };
 
 // launch helpers (kernels.cu). All enqueue on `st`; return the launch error.
@@ -178,6 +179,11 @@ cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st, b
 // kernel node of one PCG launch (args copied into the node)
 cudaError_t add_pcg_node(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode_t* deps,
                          size_t ndeps, const OpArgs& a, int nblocks);
+// the one-block control kernel after a PCG launch (OpArgs::sep), launched / as a graph node
+// after `prev` with a programmatic edge
+cudaError_t launch_pcg_red(const OpArgs& a, int nblocks, cudaStream_t st, bool pdl);
+cudaError_t add_pcg_red_node(cudaGraph_t g, cudaGraphNode_t* node, cudaGraphNode_t prev,
+                             const OpArgs& a, int nblocks);
 // the same node after `prev` with a programmatic-dependent-launch edge (prev may be null)
 cudaError_t add_pcg_node_pdl(cudaGraph_t g, cudaGraphNode_t* node, cudaGraphNode_t prev,
                              const OpArgs& a, int nblocks);

@@ -1,7 +1,7 @@
 """Device time per PCG iteration of a fixed-length solve (tol 0, N iterations) at a config,
 CUDA events around the whole tomo_solve on the bound stream (so kernel boundaries and the
 loop's own overheads are included), best of 3.
-    python scripts/time_iter.py [cfg] [iters]       (A/B knobs: TOMO_NO_PDL, TOMO_NO_GRAPH)"""
+    python scripts/time_iter.py [cfg] [iters]       (A/B knobs: TOMO_NO_PDL, TOMO_NO_GRAPH, TOMO_NO_SEP_RED)"""
 import json
 import os
 import sys
@@ -28,6 +28,6 @@ for _ in range(3):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (iters + 1)
     best = us if best is None else min(best, us)
-env = {k: os.environ[k] for k in ("TOMO_NO_PDL", "TOMO_NO_GRAPH") if k in os.environ}
+env = {k: os.environ[k] for k in ("TOMO_NO_PDL", "TOMO_NO_GRAPH", "TOMO_NO_SEP_RED") if k in os.environ}
 print(json.dumps({"cfg": cfg, "iters": iters, "us_per_iteration": round(best, 2), "env": env,
                   "lib": os.path.basename(os.environ.get("TOMO_LIB_PATH", "libtomo.so"))}))

@@ -113,6 +113,33 @@ def test_graph_and_host_batched_loops_bit_identical():
     assert torch.equal(u1, u2) and torch.equal(u1, u3) and torch.equal(dcf1, dcf2)
 
 
+@pytest.mark.parametrize("graph", [True, False])
+def test_programmatic_launch_bit_identical(graph, monkeypatch):
+    """Programmatic dependent launch (griddepcontrol.wait / launch_dependents,
+    16 PDL-chained launches per WHILE body) only changes when blocks are scheduled: the
+    iterates, count and residual history equal those of launch-to-launch order (TOMO_NO_PDL,
+    read at bind), in the graph and in host batches; max_iters not a multiple of the body."""
+    p = inputs.CFG2
+    rho = gpu(inputs.density_for("cfg2"))
+    out = []
+    for pdl in (True, False):
+        if pdl:
+            monkeypatch.delenv("TOMO_NO_PDL", raising=False)
+        else:
+            monkeypatch.setenv("TOMO_NO_PDL", "1")
+        t = tomo.Tomo(tomo.params_from_problem(p), device=DEV)
+        t.set_graph(graph)
+        h = t.set_history(600)
+        u, info = t.solve(rho, tol=1e-10, max_iters=200000)
+        u7, info7 = t.solve(rho, tol=1e-10, max_iters=37)
+        out.append((u.clone(), info, h.clone(), u7.clone(), info7))
+        t.close()
+    (u1, i1, h1, v1, j1), (u2, i2, h2, v2, j2) = out
+    assert i1.iterations == i2.iterations and i1.converged == i2.converged >= 1
+    assert torch.equal(u1, u2) and torch.equal(h1, h2)
+    assert j1.iterations == j2.iterations == 37 and j1.converged == 0 and torch.equal(v1, v2)
+
+
 @pytest.mark.parametrize("cfg", ["cfg0", "cfg2"])
 def test_exact_beta_variant_matches_textbook_count(cfg):
     """tomo_set_pcg_exact_beta(1): beta from the explicit r_{k+1} - the textbook recurrence of
