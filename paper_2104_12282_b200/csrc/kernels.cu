@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   const Grid& g = a.g;
 
   double beta = 0.0, alpha_prev = 0.0;
-  if (MODE == OP_PCG && !a.sep) {
+  if (MODE == OP_PCG && (!a.sep || TOMO_SEP_EARLY)) {
     // programmatic dependent launch: this grid may have been scheduled while the previous
     // PCG launch was finishing; everything below reads its results (no-op without PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
       issue_plane<MODE>(a, stages + ((git + s) % NS) * STAGE, &bars[(git + s) % NS], org, i0, j0,
                         kbeg - 1 + it0 + s);
   }
-  if (MODE == OP_PCG && a.sep && u0 - (kend - kbeg) == ub) {
+  if (MODE == OP_PCG && a.sep && !TOMO_SEP_EARLY && u0 - (kend - kbeg) == ub) {
     // separate reduction (OpArgs::sep): this grid was scheduled after the previous PCG
     // launch completed (the reduction kernel between them triggers it only then), so the
     // loads above already read final data while that kernel sums the partials; its alpha,
@@ -711,8 +711,13 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
 __global__ void __launch_bounds__(NT) k_pcg_red(const double* __restrict__ partials, int nb, Scal* s,
                                                 unsigned long long cond) {
   __shared__ double red[168];
+#if TOMO_SEP_EARLY
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // launch k+1 may be scheduled
+  asm volatile("griddepcontrol.wait;" ::: "memory");               // launch k complete
+#else
   asm volatile("griddepcontrol.wait;" ::: "memory");               // launch k complete
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // launch k+1 may start
+#endif
   if (*(volatile int*)&s->done) return;
   const int t = threadIdx.x;
   double tot[5] = {0.0, 0.0, 0.0, 0.0, 0.0};

@@ -143,6 +143,9 @@ constexpr bool OP_PINGPONG_PCG = TOMO_PINGPONG_PCG != 0;
 #ifndef TOMO_ACQREL_ARRIVE
 #define TOMO_ACQREL_ARRIVE 0  // A/B: last-block arrival as one acq_rel atomic (kernels.cu arrive_last)
 #endif
+#ifndef TOMO_SEP_EARLY
+#define TOMO_SEP_EARLY 0  // A/B: k_pcg_red lets the next launch be scheduled before it waits
+#endif
 #ifndef TOMO_OP_NS_APPLY
 #define TOMO_OP_NS_APPLY 6
 #endif
