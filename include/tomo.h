@@ -233,7 +233,10 @@ int tomo_set_history(tomo_ctx* ctx, double* d_hist, int n);
 int tomo_set_pcg_exact_beta(tomo_ctx* ctx, int on);
 /* PCG loop execution (default 1): 1 = the whole loop as one CUDA graph with a conditional
  * WHILE node (one launch and one read-back per solve); 0 = host-batched launches of the
- * same kernel (what ncu can profile: kernels inside conditional graphs are not captured). */
+ * same kernels (what ncu can profile: kernels inside conditional graphs are not captured).
+ * Either way an iteration is one fused operator pass (k_op<OP_PCG>) and, with programmatic
+ * dependent launch and single-pass beta, a one-block control kernel (k_pcg_red: grid totals,
+ * stop test, alpha, beta) chained to it; the iterates do not depend on the form.          */
 int tomo_set_graph(tomo_ctx* ctx, int on);
 /* times[0] = mean ms per fused PCG launch, times[1] = 0 (no separate K_B kernel), times[2]
  * = number of launches timed. Requires tomo_set_profiling(ctx, 1) before the solve.      */
