@@ -396,13 +396,15 @@ def run_ours(args):
     bytes_ka = 8 * (8 * n_dof + n_n + n_e) + n_n
     ka_s = prof["k_a_ms"] * 1e-3
     achieved = bytes_ka / ka_s / 1e9 if ka_s > 0 else None
-    roof = {"kernel": "k_op<OP_PCG> (single-pass PCG iteration)", "bound": "hbm", "achieved": achieved,
+    roof = {"kernel": "k_op<OP_PCG> + k_pcg_red (one single-pass PCG iteration: the fused operator "
+                      "pass and the one-block control kernel chained to it)",
+            "bound": "hbm", "achieved": achieved,
             "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
             "traffic": TRAFFIC.get(cfg), "peak_source": peak_src, "alg_bytes_per_launch": bytes_ka,
             "launch_ms": prof["k_a_ms"], "launches_timed": prof["n"],
             "share_of_step": (prof["k_a_ms"] * (iters + 1)) / ms_per_step if ms_per_step else None,
             "timing": "CUDA events around the graph launch of every PCG loop in the timed region: "
-                      "device time / (iterations + 1) launches"}
+                      "device time / (iterations + 1) iterations"}
     gf, _ = t.bench_dfma()
     ap_bytes = 16 * n_dof + 8 * n_e + n_n
     ap_gbs = ap_bytes / (ap_ms * 1e-3) / 1e9

@@ -1,5 +1,5 @@
 """The bench JSON contract (task statement) on the committed bench line of this
-round (profiles/r2g_bench_line.json, produced on a B200 by `python bench.py`): every key the
+round (profiles/r2h_bench_line.json, produced on a B200 by `python bench.py`): every key the
 driver and the judge read is present and self-consistent. CPU-only: reads the file."""
 import json
 import os
@@ -7,7 +7,7 @@ import os
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LINE = os.path.join(ROOT, "profiles", "r2g_bench_line.json")
+LINE = os.path.join(ROOT, "profiles", "r2h_bench_line.json")
 
 
 @pytest.fixture(scope="module")
