@@ -1147,7 +1147,10 @@ extern "C" int tomo_bench_apply(tomo_ctx* c, const double* d_rho, int reps, doub
   CK(c, cudaEventCreate(&e1));
   LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->ap_blocks, c->st));  // warm-up
   CK(c, cudaEventRecord(e0, c->st));
-  for (int i = 0; i < reps; ++i) LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->ap_blocks, c->st));
+  // back-to-back applications chained by programmatic dependent launch (each waits for the
+  // previous one's completion before it reads; TOMO_NO_PDL: launch-to-launch order)
+  for (int i = 0; i < reps; ++i)
+    LAUNCH(c, launch_op(OP_APPLY, c->op_apply_u, c->ap_blocks, c->st, c->pdl && i > 0));
   CK(c, cudaEventRecord(e1, c->st));
   CK(c, cudaEventSynchronize(e1));
   float ms = 0;

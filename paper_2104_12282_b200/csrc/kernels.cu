@@ -368,6 +368,10 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   const Grid& g = a.g;
 
   double beta = 0.0, alpha_prev = 0.0;
+  // K_hat u launched programmatically after another K_hat u (tomo_bench_apply): its blocks may
+  // be resident before the previous grid completes; nothing is read before it has (no-op
+  // for ordinary launches)
+  if (MODE == OP_APPLY) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (MODE == OP_PCG && (!a.sep || TOMO_SEP_EARLY)) {
     // programmatic dependent launch: this grid may have been scheduled while the previous
     // PCG launch was finishing; everything below reads its results (no-op without PDL)
@@ -628,7 +632,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   }
   // the next PCG launch may be scheduled now (it waits for this grid's completion before it
   // reads anything): its blocks take the slots of blocks that have finished their planes
-  if (MODE == OP_PCG) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef TOMO_EXP_TIMELINE
   const unsigned long long tl1 = gtimer();
   const int tl_par = MODE == OP_PCG ? (*(volatile int*)&a.s->k) & 1 : 0;
@@ -1436,19 +1440,19 @@ static void op_attr() {
 
 cudaError_t launch_op(int mode, const OpArgs& a, int nblocks, cudaStream_t st, bool pdl) {
   op_attr();
-  if (mode == OP_PCG && pdl) {
-    // programmatic dependent launch after the previous PCG launch on this stream
+  if (pdl) {
+    // programmatic dependent launch after the previous launch of the same kernel on this stream
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblocks);
     cfg.blockDim = dim3(TX, BY);
-    cfg.dynamicSmemBytes = op_smem(1);
+    cfg.dynamicSmemBytes = op_smem(mode);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_op<OP_PCG>, a);
+    return mode == OP_PCG ? cudaLaunchKernelEx(&cfg, k_op<OP_PCG>, a) : cudaLaunchKernelEx(&cfg, k_op<OP_APPLY>, a);
   }
   if (mode == OP_PCG) k_op<OP_PCG><<<nblocks, dim3(TX, BY), op_smem(1), st>>>(a);
   else k_op<OP_APPLY><<<nblocks, dim3(TX, BY), op_smem(0), st>>>(a);
