@@ -931,7 +931,13 @@ __global__ void k_compliance(const double* u, const int64_t* dofs, const double*
 // by warp shuffle and the lower face is carried from the previous plane, so an element
 // costs 6 loads instead of 24 gathers; lane 31 only supplies corners. ce = w^T D w.
 constexpr int SENS_X = 31, SENS_BY = 8;
-__global__ void __launch_bounds__(256) k_sens(Grid g, Walsh W, const double* __restrict__ rho,
+// 4 resident blocks per SM (62 registers, no spills) and z chunks from the resident slots:
+// cfg3 28.0 -> 26.3 us, 192x96x96 39.8 -> 29.5, 256x128x128 127.8 -> 69.8 us
+// (scripts/explore/sens_ab.sh; TOMO_SENS_MINB=1 / TOMO_SENS_OLDCHUNK=1 restore the old build)
+#ifndef TOMO_SENS_MINB
+#define TOMO_SENS_MINB 4
+#endif
+__global__ void __launch_bounds__(256, TOMO_SENS_MINB) k_sens(Grid g, Walsh W, const double* __restrict__ rho,
                                               const double* __restrict__ u,
                                               const uint8_t* __restrict__ mask, double penal,
                                               double dE, double Emin, double* __restrict__ dc,
@@ -1590,10 +1596,30 @@ cudaError_t launch_sens(const Grid& g, const Walsh& w, const double* rho, const 
                         double* dc, double* ce, double* partials, int max_blocks, Scal* s,
                         int want_energy, cudaStream_t st) {
   const int tiles = ((g.nx + SENS_X - 1) / SENS_X) * ((g.ny + SENS_BY - 1) / SENS_BY);
-  int chunks = std::max(1, std::min(g.nz, (4 * 148 + tiles - 1) / tiles));
+  // z-chunk length from the resident slots: minimise waves x (planes per chunk + 1)
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sens, 32 * SENS_BY, 0);
+  const long long slots = (long long)std::max(1, occ) * sms;
+  int zchunk = g.nz, chunks = 1;
+  long long best = -1;
+#if TOMO_SENS_OLDCHUNK
+  chunks = std::max(1, std::min(g.nz, (4 * 148 + tiles - 1) / tiles));
   chunks = std::max(1, std::min(chunks, max_blocks / std::max(1, tiles)));
-  const int zchunk = (g.nz + chunks - 1) / chunks;
+  zchunk = (g.nz + chunks - 1) / chunks;
   chunks = (g.nz + zchunk - 1) / zchunk;
+  const bool search = false;
+#else
+  const bool search = true;
+#endif
+  for (int c = 1; search && c <= g.nz; ++c) {
+    const int zc = (g.nz + c - 1) / c, cc = (g.nz + zc - 1) / zc;
+    const long long nb = (long long)tiles * cc;
+    if (want_energy && nb > max_blocks) break;
+    const long long cost = ((nb + slots - 1) / slots) * (zc + 1);
+    if (best < 0 || cost < best) { best = cost; zchunk = zc; chunks = cc; }
+  }
   if (want_energy && tiles * chunks > max_blocks) return cudaErrorInvalidValue;  // partials
   k_sens<<<tiles * chunks, dim3(32, SENS_BY), 0, st>>>(g, w, rho, u, mask, penal, dE, Emin, dc, ce,
                                                        partials, s, want_energy, zchunk);
