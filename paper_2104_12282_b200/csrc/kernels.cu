@@ -1088,6 +1088,9 @@ __global__ void __launch_bounds__(256) k_filter(Grid g, const int* __restrict__ 
 #ifndef TOMO_FT_ROWS
 #define TOMO_FT_ROWS 1  // output rows per thread for radii R <= 3 (A/B knob: 1, 2, 4; 1 measured best)
 #endif
+#ifndef TOMO_FT_ADJ
+#define TOMO_FT_ADJ 0  // ROWS > 1: a thread's output rows are adjacent (they share 2R of their 2R+1 tap rows) instead of FT_Y/ROWS apart
+#endif
 #ifndef TOMO_FT_ZMIN_R
 #define TOMO_FT_ZMIN_R 4  // z chunks are at least ZMIN_R * R + 4 planes thick (halo FMA waste)
 #endif
@@ -1126,11 +1129,13 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const _
                                                   double* __restrict__ out, int transpose,
                                                   int zchunk) {
   constexpr int FT_YT = FT_Y / ROWS, FT_T = FT_X * FT_YT;
+  constexpr int RSTEP = TOMO_FT_ADJ ? 1 : FT_YT;  // distance between a thread's output rows
   constexpr int PX = FT_X + 2 * R, PY = FT_Y + 2 * R, NA = 2 * R + 1, DMAX = 3 * R * R;
   constexpr int NL = (PX * PY + FT_T - 1) / FT_T;  // staged values per thread and plane
   __shared__ double pl[2][PY * PX];
   __shared__ double sw[MM >= 0 ? 1 : DMAX + 1];  // runtime-M weights (broadcast reads)
   const int tx = threadIdx.x, ty = threadIdx.y, t = ty * FT_X + tx;
+  const int ry = TOMO_FT_ADJ ? ty * ROWS : ty;     // the thread's first output row in the tile
   const int tiles_x = (g.nx + FT_X - 1) / FT_X, tiles = tiles_x * ((g.ny + FT_Y - 1) / FT_Y);
   const int tile = blockIdx.x % tiles, ch = blockIdx.x / tiles;
   const int x0 = (tile % tiles_x) * FT_X, y0 = (tile / tiles_x) * FT_Y;
@@ -1178,7 +1183,7 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const _
   auto flush = [&](int z, const double (&ih)[ROWS]) {
 #pragma unroll
     for (int h = 0; h < ROWS; ++h) {
-      const int y = y0 + ty + h * FT_YT;
+      const int y = y0 + ry + h * RSTEP;
       if (x < g.nx && y < g.ny && z >= z0 && z < z1) {
         const long long e = x + (long long)g.nx * y + pe * z;
         out[e] = transpose ? acc[h][0] : acc[h][0] * ih[h];
@@ -1191,7 +1196,7 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const _
   auto load_ih = [&](int z, double (&ih)[ROWS]) {
 #pragma unroll
     for (int h = 0; h < ROWS; ++h) {
-      const int y = y0 + ty + h * FT_YT;
+      const int y = y0 + ry + h * RSTEP;
       ih[h] = (!transpose && x < g.nx && y < g.ny && z >= z0 && z < z1)
                   ? __ldg(iHs + x + (long long)g.nx * y + pe * z) : 0.0;
     }
@@ -1219,8 +1224,8 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const _
           for (int dx = -R; dx <= R; ++dx) {
             const int m = dx * dx + dy * dy;
             if (m > MM) continue;
-            TCHECK((ty + h * FT_YT + R + dy) * PX + tx + R + dx < PX * PY);
-            const double v = P[(ty + h * FT_YT + R + dy) * PX + tx + R + dx];
+            TCHECK((ry + h * RSTEP + R + dy) * PX + tx + R + dx < PX * PY);
+            const double v = P[(ry + h * RSTEP + R + dy) * PX + tx + R + dx];
             if (ft_first_in_shell(dx, dy, R)) S[m] = v;
             else S[m] += v;
           }
@@ -1237,24 +1242,24 @@ __global__ void __launch_bounds__(FT_X * FT_Y / ROWS) k_filter_t(Grid g, const _
       }
     } else {
 #pragma unroll
-    for (int dy = -R; dy <= R + (ROWS - 1) * FT_YT; ++dy) {
+    for (int dy = -R; dy <= R + (ROWS - 1) * RSTEP; ++dy) {
 #pragma unroll
       for (int dx = -R; dx <= R; ++dx) {
         // column (dx, dy) of row 0 is column (dx, dy - FT_YT) of row 1
         bool rh[ROWS], any = false;
 #pragma unroll
         for (int h = 0; h < ROWS; ++h) {
-          const int dyh = dy - h * FT_YT;
+          const int dyh = dy - h * RSTEP;
           rh[h] = dyh >= -R && dyh <= R && dx * dx + dyh * dyh <= (MM >= 0 ? MM : DMAX);
           any |= rh[h];
         }
         if (!any) continue;
-        TCHECK((ty + R + dy) * PX + tx + R + dx < PX * PY);
-        const double v = P[(ty + R + dy) * PX + tx + R + dx];
+        TCHECK((ry + R + dy) * PX + tx + R + dx < PX * PY);
+        const double v = P[(ry + R + dy) * PX + tx + R + dx];
 #pragma unroll
         for (int h = 0; h < ROWS; ++h) {
           if (!rh[h]) continue;
-          const int dyh = dy - h * FT_YT;
+          const int dyh = dy - h * RSTEP;
 #pragma unroll
           for (int j = 0; j < NA; ++j) {
             const int dz = R - j, d2 = dx * dx + dyh * dyh + dz * dz;
