@@ -1073,9 +1073,9 @@ __global__ void __launch_bounds__(256) k_filter(Grid g, const int* __restrict__ 
 }
 
 // Tiled density filter for a ball-shaped tap set {d in Z^3 : |d|^2 <= M} (every cone filter
-// w = rmin - |d| > 0 is one: sqrt is monotone). A block of FT_X x FT_YT threads owns FT_X x
-// 2 FT_YT output columns (each thread two rows, y and y + FT_YT) and marches along z through
-// a chunk of planes. Each input plane (tile + R halo, zero outside the domain; multiplied by
+// w = rmin - |d| > 0 is one: sqrt is monotone). A block of FT_X x FT_Y / ROWS threads owns
+// FT_X x FT_Y output columns (each thread ROWS adjacent rows for radii R <= 3, one row beyond)
+// and marches along z through a chunk of planes. Each input plane (tile + R halo, zero outside the domain; multiplied by
 // 1/Hs in transpose mode: P^T v = H (v / Hs)) is staged once in shared memory, double
 // buffered with the next plane's global loads issued before the current plane's FMAs, and
 // scattered into 2R+1 register accumulators per output row, acc[j] = output plane zi - R + j.
@@ -1086,10 +1086,14 @@ __global__ void __launch_bounds__(256) k_filter(Grid g, const int* __restrict__ 
 #define TOMO_FT_SHELL 1  // specialised radii: shell sums (A/B knob: 0 = one FMA per tap)
 #endif
 #ifndef TOMO_FT_ROWS
-#define TOMO_FT_ROWS 1  // output rows per thread for radii R <= 3 (A/B knob: 1, 2, 4; 1 measured best)
+#define TOMO_FT_ROWS 2  // output rows per thread for radii R <= 3 (A/B knob: 1, 2, 4; 2 adjacent rows measured best)
 #endif
 #ifndef TOMO_FT_ADJ
-#define TOMO_FT_ADJ 0  // ROWS > 1: a thread's output rows are adjacent (they share 2R of their 2R+1 tap rows) instead of FT_Y/ROWS apart
+// ROWS > 1: a thread's output rows are adjacent (y, y+1: they share 2R of their 2R+1 tap rows, so
+// the shared loads per output drop from (2R+1)^2 to (2R+1)(2R+2)/2) instead of FT_Y/ROWS apart
+// (no sharing). cfg3, 93 taps: 1 row 23.4 us, 2 rows FT_Y/2 apart 33.5, 2 adjacent rows 21.2,
+// 4 adjacent rows 25.3 (64-thread blocks: too few warps) (scripts/explore/filter_ab.sh)
+#define TOMO_FT_ADJ 1
 #endif
 #ifndef TOMO_FT_ZMIN_R
 #define TOMO_FT_ZMIN_R 4  // z chunks are at least ZMIN_R * R + 4 planes thick (halo FMA waste)
