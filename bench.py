@@ -300,6 +300,13 @@ def run_reference(args):
 TRAFFIC = {"cfg3": 272688384}  # round 2: mean DRAM read + write per launch over 7 captures (profiles/r2_ncu_kernels.json)
 
 
+# thread-level DP instructions (DFMA + DADD + DMUL) per K_hat u launch from the same ncu captures
+# (profiles/r2h_ncu_kernels.json): the DP-pipe leg of the operator's roofline - one pipe slot
+# per instruction, 64 lanes per SM and clock (B200_PROFILING.md: 148 SMs), so a DADD costs
+# what a DFMA costs although it counts one flop
+DP_INST_APPLY = {"cfg3": 269.4e6}
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -428,6 +435,12 @@ def run_ours(args):
                "fp64_frac": ap_gflops / gf if gf else None,
                "roofline_frac": max(ap_bytes / (hbm * 1e9), 213 * n_e / (gf * 1e9)) / (ap_ms * 1e-3)
                if gf else None}
+    if gf and cfg in DP_INST_APPLY:
+        # gf is the measured DFMA rate (2 flop per lane-slot): lane-slots/s = gf / 2
+        dp_s = DP_INST_APPLY[cfg] / (gf * 1e9 / 2)
+        k_hat_u["dp_pipe"] = {"thread_inst": DP_INST_APPLY[cfg], "floor_us": dp_s * 1e6,
+                              "frac": dp_s / (ap_ms * 1e-3),
+                              "note": "context only: roofline_frac above is the contract's figure"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

@@ -297,9 +297,16 @@ int make_map(tomo_ctx* c, CUtensorMap* tm, CUtensorMapDataType dt, void* base, u
   const cuuint64_t strides[2] = {pitch1, pitch2};
   const cuuint32_t box[3] = {b0, b1, 1};
   const cuuint32_t es[3] = {1, 1, 1};
+  // A/B knob TOMO_TMA_L2PROMO = 0 (none) | 1 (64 B) | 2 (128 B, default) | 3 (256 B)
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  if (const char* e = getenv("TOMO_TMA_L2PROMO")) {
+    const int v = atoi(e);
+    promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+            : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+            : v == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  }
   CUresult r = fn(tm, dt, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(c, TOMO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return TOMO_OK;
 }

@@ -96,6 +96,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -115,6 +118,22 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
+
+// Tensor memory as thread-private storage (TOMO_GS_TMEM, A/B): shape 32x32b = lane l of warp w
+// reads/writes its own 32-bit cells at TMEM lane 32 (w % 4) + l, columns col .. col + 7
+__device__ __forceinline__ void tmem_ld8(unsigned taddr, unsigned (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st8(unsigned taddr, const unsigned (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -361,8 +380,10 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   double* CD = stages + NS * STAGE;          // [2][3][NT] bottom-face contributions (by parity)
   double* GS = CD + 6 * NT;                  // [GSN][NT] thread-private: top face of the last element
   double* red = GS + GSN * NT;               // [168]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 168);  // [NS]
-  int* s_flag = reinterpret_cast<int*>(bars + NS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 168);  // [NS] full (TMA bytes landed)
+  uint64_t* ebars = bars + NS;                              // [NS] empty (every warp has read the stage)
+  int* s_flag = reinterpret_cast<int*>(ebars + NS);
+  constexpr bool kEarly = MODE == OP_PCG && TOMO_EARLY_REFILL;
 
   const int tx = threadIdx.x, ty = threadIdx.y, t = ty * TX + tx;
   const Grid& g = a.g;
@@ -405,10 +426,26 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   }
 
   if (t == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NS; ++s) { mbar_init(&bars[s], 1); mbar_init(&ebars[s], BY); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  constexpr bool kGsTmem = MODE == OP_PCG && TOMO_GS_TMEM;
+  unsigned* s_tmem = reinterpret_cast<unsigned*>(s_flag + 1);
+  if (kGsTmem && ty == 0) {  // warp 0 allocates 64 TMEM columns (48 used: 2 warps per lane quarter x 24)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n" ::"r"(smem_u32(s_tmem)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  if (kGsTmem) asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if (kGsTmem) asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const unsigned tm_base = kGsTmem ? *s_tmem : 0u;
+  const unsigned tm_gs = tm_base + ((unsigned)((ty & 3) * 32) << 16) + (unsigned)(ty >> 2) * 24u;
+  auto tmem_free = [&]() {
+    if (kGsTmem) {
+      __syncthreads();
+      if (ty == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(tm_base) : "memory");
+    }
+  };
   double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // p.q, r.z, r.r, z.q, q.D^-1.q
 
   int git = 0;  // global step counter (mbarrier phase)
@@ -438,6 +475,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
       if (t == 0)  // no bulk copy may be in flight at exit
         for (int s = 0; s < NS && it0 + s < nit; ++s)
           mbar_wait(&bars[(git + s) % NS], (unsigned)((git + s) / NS) & 1u);
+      tmem_free();
       return;
     }
     beta = *(volatile double*)&a.s->beta;
@@ -535,6 +573,12 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
 #pragma unroll
     for (int c = 0; c < 3; ++c) N.pv[c] = vo[c];
     const double Ecur = stg[L::ee + fe];  // lane 31: a column outside the tile (unused)
+    if (kEarly) {
+      // the stage's last read is above: release it (one arrival per warp) so that its refill
+      // can be issued in the middle of this step instead of after the plane barrier
+      __syncwarp();
+      if (tx == 0) mbar_arrive(&ebars[s]);
+    }
 
     // ---- element row ty between node rows b and o (lane 31's results are never read;
     // skipping out-of-domain rows of edge tiles measured slower: 79.8 vs 78.4 us)
@@ -551,6 +595,10 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
       N.F[6 + c] = dl + dln;
       N.F[9 + c] = dln - dl;
     }
+    if (kEarly && t == 0 && it + NS < nit) {
+      mbar_wait(&ebars[s], (unsigned)((git - 1) / NS) & 1u);  // all BY warps have read stage s
+      issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
+    }
     double cup[3] = {0.0, 0.0, 0.0};
     if (it >= 1) {
       double Gb[12], Gt[12];
@@ -561,13 +609,29 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
       element_core(P.F, N.F, Ecur, a.w, Gb, Gt);
 #endif
       if (it >= 2) {
+        if (kGsTmem) tmem_wait_st();  // the previous step's top face is in tensor memory
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           // previous element's top face + this element's bottom face, in face modes
-          const double m00 = (kGsReg ? P.G[0 + c] : GS[(0 + c) * NT + t]) + Gb[0 + c];
-          const double m10 = (kGsReg ? P.G[3 + c] : GS[(3 + c) * NT + t]) + Gb[3 + c];
-          const double m01 = (kGsReg ? P.G[6 + c] : GS[(6 + c) * NT + t]) + Gb[6 + c];
-          const double m11 = (kGsReg ? P.G[9 + c] : GS[(9 + c) * NT + t]) + Gb[9 + c];
+          double g00, g10, g01, g11;
+          if (kGsTmem) {
+            unsigned r[8];
+            tmem_ld8(tm_gs + 8u * c, r);
+            tmem_wait_ld();
+            g00 = __hiloint2double((int)r[1], (int)r[0]);
+            g10 = __hiloint2double((int)r[3], (int)r[2]);
+            g01 = __hiloint2double((int)r[5], (int)r[4]);
+            g11 = __hiloint2double((int)r[7], (int)r[6]);
+          } else {
+            g00 = kGsReg ? P.G[0 + c] : GS[(0 + c) * NT + t];
+            g10 = kGsReg ? P.G[3 + c] : GS[(3 + c) * NT + t];
+            g01 = kGsReg ? P.G[6 + c] : GS[(6 + c) * NT + t];
+            g11 = kGsReg ? P.G[9 + c] : GS[(9 + c) * NT + t];
+          }
+          const double m00 = g00 + Gb[0 + c];
+          const double m10 = g10 + Gb[3 + c];
+          const double m01 = g01 + Gb[6 + c];
+          const double m11 = g11 + Gb[9 + c];
           // inverse transform: the x butterfly first (corner x = 1 of element tx-1 comes from
           // the lane below), then the y butterfly of the node column (8 DADD per component)
           const double L0 = m00 - m10, L1 = m01 - m11, R0 = m00 + m10, R1 = m01 + m11;
@@ -577,15 +641,28 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
           CDn[c * NT + t] = c0 - c1;   // -> node row b
         }
       }
+      if (kGsTmem) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          unsigned r[8];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            r[2 * m] = (unsigned)__double2loint(Gt[3 * m + c]);
+            r[2 * m + 1] = (unsigned)__double2hiint(Gt[3 * m + c]);
+          }
+          tmem_st8(tm_gs + 8u * c, r);
+        }
+      } else {
 #pragma unroll
       for (int i = 0; i < 12; ++i) {
         if (kGsReg) N.G[i] = Gt[i];
         else GS[i * NT + t] = Gt[i];
       }
+      }
     }
     __syncthreads();  // CD of this plane complete; stage s consumed by every warp
     // (issuing from warp BY-1, which has no owned row, measured the same: 71.8 vs 71.4 us)
-    if (t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
+    if (!kEarly && t == 0 && it + NS < nit) issue_plane<MODE>(a, stg, &bars[s], org, i0, j0, kn + NS);
     // (a segment's last NS steps issue nothing, so the next segment starts with free stages)
 
     if (it >= 2 && mine) {
@@ -633,6 +710,7 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
   // the next PCG launch may be scheduled now (it waits for this grid's completion before it
   // reads anything): its blocks take the slots of blocks that have finished their planes
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  tmem_free();
 #ifdef TOMO_EXP_TIMELINE
   const unsigned long long tl1 = gtimer();
   const int tl_par = MODE == OP_PCG ? (*(volatile int*)&a.s->k) & 1 : 0;
@@ -1435,7 +1513,7 @@ int op_tiles(const Grid& g) {
 
 size_t op_smem(int mode) {
   const size_t ns = mode == OP_PCG ? NS : NS_A, st = mode == OP_PCG ? STAGE : STAGE_A;
-  return sizeof(double) * (ns * st + (6 + GSN) * NT + 168) + sizeof(uint64_t) * ns + 16;
+  return sizeof(double) * (ns * st + (6 + GSN) * NT + 168) + sizeof(uint64_t) * 2 * ns + 16;
 }
 
 // The dynamic shared memory opt-in is a per-device function attribute: set it once per

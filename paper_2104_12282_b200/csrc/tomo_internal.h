@@ -149,6 +149,12 @@ constexpr bool OP_PINGPONG_PCG = TOMO_PINGPONG_PCG != 0;
 #ifndef TOMO_OP_NS_APPLY
 #define TOMO_OP_NS_APPLY 6
 #endif
+#ifndef TOMO_GS_TMEM
+#define TOMO_GS_TMEM 0  // A/B: the PCG kernel's top-face carry in tensor memory instead of shared memory
+#endif
+#ifndef TOMO_EARLY_REFILL
+#define TOMO_EARLY_REFILL 0  // A/B: PCG stage refill issued mid-step behind an "empty" mbarrier
+#endif
 constexpr int OP_NS_APPLY = TOMO_OP_NS_APPLY;  // stages of the K_hat u kernel (smaller stages)
 // (an L2 prefetch of planes 2-6 ahead measured slower at every distance: 82.5-106.5 vs 79.8 us)
 
