@@ -971,8 +971,12 @@ int evaluate_dev(tomo_ctx* c, const double* d_rho, double* d_u, double* d_dc, do
   if (it < 0) return it;
   double* dc = d_dc ? d_dc : c->t0();
   LAUNCH(c, launch_compliance(d_u, c->ld(), c->lv(), (int)c->load_dofs.size(), c->scal(), c->st));
-  LAUNCH(c, launch_sens(c->g, c->w, d_rho, d_u, c->dmask(), c->penal, c->E0 - c->Emin, c->Emin,
-                        dc, nullptr, c->part(), (int)c->n_part, c->scal(), 0, c->st));
+  // the solve left u in the workspace in the padded row-SoA layout (zero at fixed DOFs):
+  // the sensitivity reads that copy (coalesced, no mask bytes) instead of the dense d_u
+  // (not when f = 0: tomo_solve then returns u = 0 without touching the workspace copy)
+  const bool pad_u = c->fnorm != 0.0 && !getenv("TOMO_SENS_DENSE");  // A/B knob
+  LAUNCH(c, launch_sens(c->g, c->w, d_rho, pad_u ? c->u() : d_u, pad_u ? nullptr : c->dmask(), c->penal,
+                        c->E0 - c->Emin, c->Emin, dc, nullptr, c->part(), (int)c->n_part, c->scal(), 0, c->st));
   LAUNCH(c, run_filter(c, dc, d_dcf, 1));
   if (c_out) {
     CK(c, cudaMemcpyAsync(c_out, &c->scal()->comp, sizeof(double), cudaMemcpyDeviceToHost, c->st));

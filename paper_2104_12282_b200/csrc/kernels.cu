@@ -1008,6 +1008,7 @@ __global__ void k_compliance(const double* u, const int64_t* dofs, const double*
 // node plane is loaded once per thread (6 values, masked), the x-neighbour's corners come
 // by warp shuffle and the lower face is carried from the previous plane, so an element
 // costs 6 loads instead of 24 gathers; lane 31 only supplies corners. ce = w^T D w.
+// mask == nullptr: u is the workspace's padded row-SoA solution (coalesced, no mask bytes).
 constexpr int SENS_X = 31, SENS_BY = 8;
 // 4 resident blocks per SM (62 registers, no spills) and z chunks from the resident slots:
 // cfg3 28.0 -> 26.3 us, 192x96x96 39.8 -> 29.5, 256x128x128 127.8 -> 69.8 us
@@ -1036,7 +1037,17 @@ __global__ void __launch_bounds__(256, TOMO_SENS_MINB) k_sens(Grid g, Walsh W, c
   double Flo[12], Fhi[12];
   auto face = [&](int k, double (&F)[12]) {  // Walsh face of node plane k for element (i, j)
     double a0[3] = {0.0, 0.0, 0.0}, a1[3] = {0.0, 0.0, 0.0};
-    if (node_ok) {
+    if (node_ok && mask == nullptr) {
+      // u in the internal padded row-SoA layout (zero at fixed DOFs): one component of 32
+      // consecutive nodes per load instruction, no mask bytes (tomo_evaluate's path)
+      const long long b0 = dof_pad(g, in, j, k, 0);
+      TCHECK(b0 >= 0 && b0 + 5LL * g.nnx_pad < g.ndof_pad && k <= g.nz);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a0[c] = __ldg(u + b0 + (long long)c * g.nnx_pad);
+        a1[c] = __ldg(u + b0 + (long long)(3 + c) * g.nnx_pad);
+      }
+    } else if (node_ok) {
       const long long n0 = node_dense(g, in, j, k), n1 = node_dense(g, in, j + 1, k);
       TCHECK(n0 >= 0 && n1 < g.nn && k <= g.nz);
       const unsigned m0 = __ldg(mask + mask_index(g, in, j, k));
