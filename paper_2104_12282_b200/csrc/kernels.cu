@@ -1013,6 +1013,9 @@ constexpr int SENS_X = 31, SENS_BY = 8;
 // 4 resident blocks per SM (62 registers, no spills) and z chunks from the resident slots:
 // cfg3 28.0 -> 26.3 us, 192x96x96 39.8 -> 29.5, 256x128x128 127.8 -> 69.8 us
 // (scripts/explore/sens_ab.sh; TOMO_SENS_MINB=1 / TOMO_SENS_OLDCHUNK=1 restore the old build)
+#ifndef TOMO_SENS_PREFETCH
+#define TOMO_SENS_PREFETCH 0  // A/B: node-plane loads issued one plane ahead of use
+#endif
 #ifndef TOMO_SENS_MINB
 #define TOMO_SENS_MINB 4
 #endif
@@ -1035,8 +1038,10 @@ __global__ void __launch_bounds__(256, TOMO_SENS_MINB) k_sens(Grid g, Walsh W, c
   const int ipen = (penal == (double)(int)penal && penal >= 1.0 && penal <= 8.0) ? (int)penal : 0;
   double energy = 0.0;
   double Flo[12], Fhi[12];
-  auto face = [&](int k, double (&F)[12]) {  // Walsh face of node plane k for element (i, j)
-    double a0[3] = {0.0, 0.0, 0.0}, a1[3] = {0.0, 0.0, 0.0};
+  // raw corner values of node plane k: this lane's node column, rows j and j+1
+  auto load = [&](int k, double (&a0)[3], double (&a1)[3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { a0[c] = 0.0; a1[c] = 0.0; }
     if (node_ok && mask == nullptr) {
       // u in the internal padded row-SoA layout (zero at fixed DOFs): one component of 32
       // consecutive nodes per load instruction, no mask bytes (tomo_evaluate's path)
@@ -1058,6 +1063,8 @@ __global__ void __launch_bounds__(256, TOMO_SENS_MINB) k_sens(Grid g, Walsh W, c
         a1[c] = ((m1 >> c) & 1u) ? 0.0 : __ldg(u + 3 * n1 + c);
       }
     }
+  };
+  auto face = [&](const double (&a0)[3], const double (&a1)[3], double (&F)[12]) {  // Walsh face
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double b0 = __shfl_down_sync(0xffffffffu, a0[c], 1);
@@ -1065,9 +1072,22 @@ __global__ void __launch_bounds__(256, TOMO_SENS_MINB) k_sens(Grid g, Walsh W, c
       face_from(a0[c], b0, a1[c], b1, F, c);
     }
   };
-  face(k0, Flo);
+  double A0[3], A1[3];
+  load(k0, A0, A1);
+  face(A0, A1, Flo);
+#if TOMO_SENS_PREFETCH
+  load(k0 + 1, A0, A1);  // k0 + 1 <= nz
+#endif
   for (int k = k0; k < k1; ++k) {
-    face(k + 1, Fhi);
+#if TOMO_SENS_PREFETCH
+    // plane k+1 was loaded one step earlier; the loads of plane k+2 fly during this element
+    double B0[3], B1[3];
+    if (k + 1 < k1) load(k + 2, B0, B1);
+    face(A0, A1, Fhi);
+#else
+    load(k + 1, A0, A1);
+    face(A0, A1, Fhi);
+#endif
     if (elem_ok) {
       const long long e = in + (long long)g.nx * (j + (long long)g.ny * k);
       const double ce = element_energy(Flo, Fhi, W);
@@ -1087,6 +1107,12 @@ __global__ void __launch_bounds__(256, TOMO_SENS_MINB) k_sens(Grid g, Walsh W, c
     }
 #pragma unroll
     for (int q = 0; q < 12; ++q) Flo[q] = Fhi[q];
+#if TOMO_SENS_PREFETCH
+    if (k + 1 < k1) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { A0[c] = B0[c]; A1[c] = B1[c]; }
+    }
+#endif
   }
   if (!want_energy) return;
   const double bs = block_sum(energy, red);
