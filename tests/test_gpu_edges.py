@@ -138,6 +138,28 @@ def test_evaluation_and_oc_bitwise_deterministic():
     assert torch.equal(a[4], b[4]) and a[5] == b[5] and a[6] == b[6]
 
 
+@pytest.mark.parametrize("dims", [(24, 12, 12), (31, 9, 7), (33, 8, 5)])
+def test_evaluate_sensitivity_on_padded_u_matches_dense_path(dims, monkeypatch):
+    """tomo_evaluate's sensitivity reads the workspace's padded row-SoA solution; the dense
+    path (TOMO_SENS_DENSE, what tomo_sensitivity does with a caller's u) must give the same dc
+    bit for bit, and both match the oracle on the returned u (ragged tiles included)."""
+    p = inputs.Problem("s", *dims, rmin=1.5)
+    rho_np = np.random.default_rng(11).uniform(0.05, 1.0, p.n_elem)
+    rho = gpu(rho_np)
+    t = tomo.Tomo(tomo.params_from_problem(p), device=DEV)
+    dc_pad, dc_dense = t.zeros_elem(), t.zeros_elem()
+    u, c, dcf, info = t.evaluate(rho, None, dc_pad, None)
+    monkeypatch.setenv("TOMO_SENS_DENSE", "1")
+    u2, c2, dcf2, info2 = t.evaluate(rho, None, dc_dense, None)
+    monkeypatch.delenv("TOMO_SENS_DENSE")
+    assert torch.equal(u, u2) and torch.equal(dc_pad, dc_dense) and torch.equal(dcf, dcf2)
+    assert torch.equal(dc_pad, t.sensitivity(rho, u))
+    op = OracleProblem(p)
+    # same u on both sides; a solved u makes u_e^T KE u_e a difference of large nearly equal
+    # displacements, so the two summation orders differ by a few 1e-12 (measured 3e-12 - 5e-12)
+    assert rel(cpu(dc_pad), op.sensitivity(rho_np, cpu(u))[0]) <= 1e-10
+
+
 def test_paper_scale_filter_on_mesh3_sampled():
     """SURVEY f3 at full size: the paper's R = 0.08 on the inferred Mesh 3 (180x90x90, 1.46M
     elements, 7.2 elements = 1551 taps). The oracle cannot form P here
