@@ -340,13 +340,19 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    ap_first = None
+    ap_first = gf_burst = None
     for w in range(args.warmup):
         _, c, _, info = step()
         if w == 0:
-            # K_hat u right after the first warm-up evaluation (a realistic u, < 1 s of load):
-            # the box's power cap has not yet pulled the SM clock down (burst conditions)
+            # K_hat u timed alone in burst conditions: on the converged u of the first warm-up
+            # evaluation, after a 3 s pause that lets the SM clock return from the power-capped
+            # state the solve leaves (measured: 31.0 us at 1965 MHz after the pause, 32.6-34.5 us
+            # right after solves at 1780-1870 MHz, same u; profiles/r2x_apply_data_clock.jsonl).
+            # The remaining warm-ups follow, so the timed region starts in the sustained state.
+            torch.cuda.synchronize()
+            time.sleep(3.0)
             ap_first = min(t.bench_apply(rho, reps=200) for _ in range(3))
+            gf_burst, _ = t.bench_dfma()  # the FP64 rate in the same (burst) conditions
     # ---- standalone K_hat u (BJ metric's second half), timed alone before the timed
     # evaluations: the best of 3 means of 200 back-to-back launches of the operator kernel on
     # the workspace's internal u (the last warm-up solution) and the same rho, outside the
@@ -424,12 +430,16 @@ def run_ours(args):
             "timing": "CUDA events around the graph launch of every PCG loop in the timed region: "
                       "device time / (iterations + 1) iterations"}
     gf, _ = t.bench_dfma()
+    if ap_first and ap_first <= ap_sustained and gf_burst:
+        gf = gf_burst  # K_hat u's FP64 legs against the rate measured next to it
     ap_bytes = 16 * n_dof + 8 * n_e + n_n
     ap_gbs = ap_bytes / (ap_ms * 1e-3) / 1e9
     ap_gflops = 213 * n_e / (ap_ms * 1e-3) / 1e9
     k_hat_u = {"kernel": "k_op<OP_APPLY>", "us": ap_ms * 1e3,
-               "us_after_first_warmup": ap_first * 1e3 if ap_first else None,
+               "us_burst": ap_first * 1e3 if ap_first else None,
                "us_after_all_warmups": ap_sustained * 1e3, "applications_per_s": 1e3 / ap_ms,
+               "conditions": "us = the burst figure (kernel timed alone after a 3 s pause, SM clock "
+                             "recovered); us_after_all_warmups = right after the sustained warm-up solves",
                "dof_updates_per_s": n_dof * 1e3 / ap_ms, "alg_bytes": ap_bytes, "achieved_gbs": ap_gbs,
                "hbm_frac": ap_gbs / hbm, "gflops": ap_gflops, "fp64_peak_gflops": gf,
                "fp64_frac": ap_gflops / gf if gf else None,
