@@ -536,10 +536,12 @@ int build_op_args(tomo_ctx* c) {
   c->op_apply_u.zchunks = c->ap_zchunks;
   c->op_apply_u.tm_in = tm_u;
   c->op_apply_u.out = c->q(0);
+  c->op_apply_u.u = c->u();      // APPLY: the input vector itself (raw values at fixed DOFs)
   c->op_apply_p0 = base;
   c->op_apply_p0.zchunks = c->ap_zchunks;
   c->op_apply_p0.tm_in = tm_p[0];
   c->op_apply_p0.out = c->q(0);
+  c->op_apply_p0.u = c->p(0);
   // launch k reads the "old" buffers (k & 1) ^ 1 and writes the "new" ones k & 1
   for (int par = 0; par < 2; ++par) {
     const int o = par ^ 1, n = par;
@@ -1243,9 +1245,11 @@ int mg_build_maps(tomo_ctx* c) {
   c->op_apply_P = c->op_apply_u;
   c->op_apply_P.tm_in = tP;
   c->op_apply_P.out = P(c->mg_off_Q);
+  c->op_apply_P.u = P(c->mg_off_P);
   c->op_apply_Z = c->op_apply_u;
   c->op_apply_Z.tm_in = tZ;
   c->op_apply_Z.out = c->q(0);
+  c->op_apply_Z.u = P(c->mg_off_Z);
   return TOMO_OK;
 }
 

@@ -566,8 +566,13 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         vb[c] = ((mb >> c) & 1u) ? 0.0 : stg[R_OFF + fvb + c * VB_W];
+#if TOMO_APPLY_RAWLDG
+        // (raw u of a fixed DOF is re-read from global memory at the output instead of carried)
+        vo[c] = ((N.pm >> c) & 1u) ? 0.0 : stg[R_OFF + fvo + c * VB_W];
+#else
         N.pz[c] = stg[R_OFF + fvo + c * VB_W];  // raw u (identity rows at fixed DOFs)
         vo[c] = ((N.pm >> c) & 1u) ? 0.0 : N.pz[c];
+#endif
       }
     }
 #pragma unroll
@@ -682,7 +687,11 @@ __global__ void __launch_bounds__(NT, MODE == OP_PCG ? OP_MINB : OP_MINB_APPLY)
           zq = fma(P.pz[c], qv, zq);
           qdq = fma(P.pdi * qv, qv, qdq);
         } else {
+#if TOMO_APPLY_RAWLDG
+          a.out[gb + c * g.nnx_pad] = fixed ? __ldg(a.u + gb + c * g.nnx_pad) : qv;
+#else
           a.out[gb + c * g.nnx_pad] = fixed ? P.pz[c] : qv;
+#endif
         }
       }
       acc[0] += pq;

@@ -149,6 +149,9 @@ constexpr bool OP_PINGPONG_PCG = TOMO_PINGPONG_PCG != 0;
 #ifndef TOMO_OP_NS_APPLY
 #define TOMO_OP_NS_APPLY 6
 #endif
+#ifndef TOMO_APPLY_RAWLDG
+#define TOMO_APPLY_RAWLDG 0  // A/B: K_hat u re-reads the raw u of fixed DOFs at the output (no carry)
+#endif
 #ifndef TOMO_GS_TMEM
 #define TOMO_GS_TMEM 0  // A/B: the PCG kernel's top-face carry in tensor memory instead of shared memory
 #endif
@@ -170,7 +173,7 @@ struct OpArgs {
   Walsh w;
   double* rnew;         // PCG: r_k (owned nodes written)
   double* pnew;         // PCG: p_k (owned nodes written)
-  double* u;            // PCG: u (owned nodes: u += alpha_{k-1} p_{k-1})
+  double* u;            // PCG: u (owned nodes: u += alpha_{k-1} p_{k-1}) ; APPLY: the input vector
   double* out;          // APPLY: y (raw u at fixed DOFs) ; PCG: q
   double* partials;     // PCG: five per block
   Scal* s;              // PCG
