@@ -61,6 +61,7 @@ struct tomo_ctx {
   int sms = 148;
   // operator launch variants (tensor maps bound to workspace buffers)
   OpArgs op_apply_u{}, op_apply_p0{}, op_pcg[2];  // op_pcg[k & 1] for launch k
+  cudaAccessPolicyWindow l2win{};  // TOMO_L2_PERSIST (A/B): persisting window of the PCG launches; num_bytes 0 = none
   cudaGraph_t pcg_graph = nullptr;        // WHILE(not done) { launch even; launch odd }
   bool use_graph = true;                  // tomo_set_graph: graph (1) or host batches (0)
   bool exact_beta = false;                // tomo_set_pcg_exact_beta: textbook beta (extra pass)
@@ -435,12 +436,12 @@ extern "C" int tomo_create(tomo_ctx** out, const tomo_grid* gr, double E0, doubl
   const size_t vp = sizeof(double) * (size_t)g.ndof_pad, ve = sizeof(double) * (size_t)g.ne;
   c->off_E = take(sizeof(double) * (size_t)g.ne_pad);
   c->off_dinv = take(sizeof(double) * (size_t)g.nn_pad);
+  c->off_u = take(vp);  // next to E and D^-1: one contiguous L2 access-policy window (tomo_bind)
   c->off_Hs = take(ve);
   c->off_iHs = take(ve);
   c->off_t0 = take(ve);
   c->off_t1 = take(ve);
   c->off_t2 = take(ve);
-  c->off_u = take(vp);
   c->off_r0 = take(vp);
   c->off_r1 = take(vp);
   c->off_p0 = take(vp);
@@ -567,6 +568,14 @@ namespace {
 // The whole PCG loop as one graph: a conditional WHILE node whose body is the even and the
 // odd launch; the last block of a launch that sets `done` clears the condition. Launches
 // after convergence inside the body exit at their first instruction.
+// TOMO_L2_PERSIST: the persisting window on a PCG kernel node of the graph (no-op otherwise)
+cudaError_t l2_node(tomo_ctx* c, cudaGraphNode_t n) {
+  if (!c->l2win.num_bytes) return cudaSuccess;
+  cudaKernelNodeAttrValue v = {};
+  v.accessPolicyWindow = c->l2win;
+  return cudaGraphKernelNodeSetAttribute(n, cudaKernelNodeAttributeAccessPolicyWindow, &v);
+}
+
 int build_pcg_graph(tomo_ctx* c) {
   if (c->pcg_exec) { cudaGraphExecDestroy(c->pcg_exec); c->pcg_exec = nullptr; }
   if (c->pcg_graph) { cudaGraphDestroy(c->pcg_graph); c->pcg_graph = nullptr; }
@@ -602,6 +611,7 @@ int build_pcg_graph(tomo_ctx* c) {
       cudaGraphNode_t n;
       const OpArgs& ai = (i & 1) ? a1 : a0;
       CK(c, add_pcg_node_pdl(body, &n, prev, ai, c->op_blocks));
+      CK(c, l2_node(c, n));
       prev = n;
       if (ai.sep) {
         CK(c, add_pcg_red_node(body, &n, prev, ai, c->op_blocks));
@@ -611,13 +621,16 @@ int build_pcg_graph(tomo_ctx* c) {
     c->body_launches = U;
   } else {
   CK(c, add_pcg_node(body, &n0, nullptr, 0, a0, c->op_blocks));
+  CK(c, l2_node(c, n0));
   if (c->exact_beta) {
     cudaGraphNode_t b0, b1;
     CK(c, add_beta_node(body, &b0, &n0, 1, c->g, c->r(0), c->q(0), c->dinv(), c->scal(), c->part(), c->nb_b));
     CK(c, add_pcg_node(body, &n1, &b0, 1, a1, c->op_blocks));
+    CK(c, l2_node(c, n1));
     CK(c, add_beta_node(body, &b1, &n1, 1, c->g, c->r(1), c->q(1), c->dinv(), c->scal(), c->part(), c->nb_b));
   } else {
     CK(c, add_pcg_node(body, &n1, &n0, 1, a1, c->op_blocks));
+    CK(c, l2_node(c, n1));
   }
   }
   CK(c, cudaGraphInstantiate(&c->pcg_exec, c->pcg_graph, 0));
@@ -704,6 +717,28 @@ extern "C" int tomo_bind(tomo_ctx* c, void* d_ws, size_t bytes, void* stream) {
   c->nb_oc = std::min(oc_max_blocks(), (int)std::max<long long>(1, (g.ne + 255) / 256));
   if ((size_t)c->nb_oc * 2 > c->n_part) c->nb_oc = (int)(c->n_part / 2);
   if (int rc = build_op_args(c)) return rc;
+  c->l2win = cudaAccessPolicyWindow{};
+  if (std::getenv("TOMO_L2_PERSIST")) {
+    // A/B experiment: E and D^-1 (adjacent in the workspace, read by every PCG launch) as a
+    // persisting L2 access-policy window of the stream and of the graph's PCG kernel nodes
+    // (TOMO_L2_PERSIST=2: and u, which follows them: read and rewritten by every launch)
+    const bool with_u = atoi(std::getenv("TOMO_L2_PERSIST")) >= 2;
+    const size_t bytes = with_u ? (size_t)(c->off_u - c->off_E) + sizeof(double) * (size_t)g.ndof_pad
+                                : (size_t)(c->off_u - c->off_E);
+    int dev = 0, maxp = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(bytes + (4u << 20), (size_t)maxp));
+    fprintf(stderr, "[tomo] L2 persisting window %.1f MB (device max %.1f MB)\n", bytes / 1e6, maxp / 1e6);
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = c->E();
+    v.accessPolicyWindow.num_bytes = bytes;
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxp / (double)bytes);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CK(c, cudaStreamSetAttribute(c->st, cudaStreamAttributeAccessPolicyWindow, &v));
+    c->l2win = v.accessPolicyWindow;  // the graph's PCG kernel nodes get the same window
+  }
   if (int rc = build_pcg_graph(c)) return rc;
   CK(c, cudaStreamSynchronize(c->st));
   c->bound = true;
